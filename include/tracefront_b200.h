@@ -1,0 +1,173 @@
+/*
+ * tracefront_b200.h — C ABI of the B200-native multifrontal factor/solve path.
+ *
+ * This is the drop-in boundary for the reference package `tracefront`
+ * (/root/reference/pkg/src/tracefront).  The reference is pure Python and
+ * has no FFI; each entry point below names the reference function whose
+ * semantics it replaces (file:line).  All pointers are plain host or CUDA
+ * device pointers, sizes are int64, streams are `cudaStream_t` passed as
+ * `void*`.  No torch types cross this boundary.  The library owns only the
+ * host-side symbolic plan (`tf_plan`); every device buffer is allocated by
+ * the caller.
+ *
+ * Status codes: TF_OK (0), TF_ZERO_PIVOT (2, mirrors ZeroPivotError /
+ * cli.py exit code 2), negative values for invalid input or CUDA errors.
+ */
+#ifndef TRACEFRONT_B200_H
+#define TRACEFRONT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_OK 0
+#define TF_ZERO_PIVOT 2
+#define TF_ERR_INVALID (-1)
+#define TF_ERR_CUDA (-2)
+#define TF_ERR_STRAY (-3) /* pivot couples outside its front (tasks.py:136-140) */
+
+/* Pattern table row layout (int32 x TF_PAT_WIDTH per pattern). */
+#define TF_PAT_WIDTH 8
+#define TF_PAT_M 0      /* front order (non-eliminated indices) */
+#define TF_PAT_K 1      /* pivots eliminated in this front */
+#define TF_PAT_NSRC 2   /* 1 (element or carry child) or 2 children */
+#define TF_PAT_LEN0 3   /* length of source 0 (element size, or child m-k) */
+#define TF_PAT_LEN1 4
+#define TF_PAT_OFF0 5   /* offset of source-0 map in the maps array */
+#define TF_PAT_OFF1 6
+#define TF_PAT_LEAF 7   /* 1 when source 0 is an element matrix */
+
+/* ------------------------------------------------------------------ mesh */
+
+/* Tensor-product Q_p mesh on the unit box, DOFs numbered by the Morton index
+ * of their owning element; elements returned in Morton
+ * order, element-local DOF order x fastest.  For dim == 1 this equals
+ * fem.py:59-80 (Mesh.element_dofs).  Pass elem_dofs == NULL to query
+ * n_dof / n_elem only.  elem_dofs: n_elem * (p+1)^dim int32 (1-based). */
+int tf_mesh_tensor(int32_t dim, const int64_t* ns, int32_t degree, int64_t* n_dof,
+                   int64_t* n_elem, int32_t* elem_dofs);
+
+/* -------------------------------------------------------------- symbolic */
+
+typedef struct tf_plan tf_plan;
+
+typedef struct {
+  int64_t n_dof;
+  int64_t n_leaves;
+  int64_t n_nodes;
+  int64_t n_pivots;
+  int32_t n_levels;
+  int32_t max_m;
+  int32_t max_k;
+  int32_t keep_lists;
+} tf_plan_summary;
+
+/* Host-side per-level tables (owned by the plan; valid until destroy). */
+typedef struct {
+  int32_t level;
+  int32_t n_fronts;
+  int32_t n_patterns;
+  int32_t max_m;
+  int32_t max_k;
+  int32_t max_upd; /* max (m-k) */
+  int64_t node_base;   /* reference node id of front 0 (tree.py:133,153) */
+  int64_t piv_base;    /* first pivot-order position of this level */
+  int64_t n_pivots;    /* pivots eliminated at this level */
+  int64_t maps_len;
+  const int32_t* pattern_of; /* [n_fronts] */
+  const int64_t* piv_off;    /* [n_fronts] absolute pivot-order offset */
+  const int32_t* pat;        /* [n_patterns * TF_PAT_WIDTH] */
+  const int32_t* maps;       /* [maps_len] source position -> front position */
+} tf_level_host;
+
+/* Replaces sort_fronts + build_elimination_tree + symbolic_eliminate
+ * (tree.py:44-48, 106-160; tasks.py:88-159) for fronts given in sorted
+ * (leaf) order.  elem_ptr may be NULL when every element has nloc DOFs.
+ * keep_lists != 0 keeps the per-node [eliminable | shared] index lists
+ * (NodeReorder, tasks.py:62-70) for parity queries. */
+int tf_plan_create(int64_t n_dof, int64_t n_elem, const int64_t* elem_ptr, int32_t nloc,
+                   const int32_t* elem_dofs, int32_t keep_lists, tf_plan** out);
+void tf_plan_destroy(tf_plan* plan);
+int tf_plan_summary_get(const tf_plan* plan, tf_plan_summary* out);
+int tf_plan_level(const tf_plan* plan, int32_t level, tf_level_host* out);
+/* EliminationPlan.pivot_order (tasks.py:83-85): n_pivots 1-based DOFs. */
+int tf_plan_pivot_order(const tf_plan* plan, int32_t* out);
+/* Per-node front lists of one level: ptr[n_fronts+1], k[n_fronts], idx[ptr[n]]
+ * ([eliminable ascending | shared ascending], tasks.py:114-122). */
+int tf_plan_node_lists(const tf_plan* plan, int32_t level, int64_t* ptr, int32_t* k,
+                       int32_t* idx);
+/* Total length of the node lists of one level. */
+int64_t tf_plan_node_lists_len(const tf_plan* plan, int32_t level);
+
+/* ---------------------------------------------------------------- device */
+
+/* Device view of one level: the tf_level_host arrays copied to the GPU. */
+typedef struct {
+  int32_t level;
+  int32_t n_fronts;
+  int32_t n_patterns;
+  int32_t max_m;
+  int32_t max_k;
+  int32_t max_upd;
+  int32_t is_leaf;
+  int32_t elem_ld;          /* leading dimension of element matrices (leaf level) */
+  int64_t fac_stride;       /* doubles per front slot in the factor buffer (>= m*k) */
+  int64_t upd_stride;       /* doubles per front slot in this level's update buffer */
+  int64_t child_upd_stride; /* upd_stride of level-1 (0 at the leaf level) */
+  int64_t elem_stride;      /* doubles between element matrices (0: uniform) */
+  const int32_t* pattern_of;
+  const int64_t* piv_off;
+  const int32_t* pat;
+  const int32_t* maps;
+} tf_level_view;
+
+/* Workspace bytes tf_level_factor needs for this level (0 for small fronts). */
+int64_t tf_level_factor_workspace(const tf_level_view* lv);
+
+/* One Foata class (tree level) of the numeric factorization: extend-add of
+ * children update matrices (or element matrices at the leaves), partial
+ * LDL^T of the k fully-summed pivots, Schur complement.  Replaces the
+ * Division/Multiplication/Subtraction tasks of one level (engine.py:78-107,
+ * 290-306) and factorize_nested_loops' per-level loop (engine.py:518-547).
+ * factors: n_fronts * fac_stride (row-major m x k panel per front: the
+ * strictly-lower part holds l(x,z) = u(z,x), the diagonal holds u(z,z)).
+ * upd_out: n_fronts * upd_stride (packed lower (m-k)^2 Schur complement).
+ * err: device uint64, atomicMin of the pivot-order position of the first
+ * pivot with |d| <= threshold (engine.py:91-92, 158-159, 529-530). */
+int tf_level_factor(const tf_level_view* lv, const double* child_upd, const double* elem,
+                    double* factors, double* upd_out, double threshold,
+                    unsigned long long* err, void* workspace, int64_t workspace_bytes,
+                    void* stream);
+
+/* Forward sweep of solve (engine.py:481-487) for one level, nrhs columns,
+ * row-major (n x nrhs) vectors in pivot order.  child: view of level-1 (NULL
+ * at the leaves); w_child: its front blocks (stride child_rows * nrhs, update
+ * rows start at the child's k); w_out: this level's front blocks (stride
+ * out_rows * nrhs, out_rows >= max_m); y: pivot-order RHS, overwritten by
+ * D^-1 L^-1 b at this level's pivots. */
+int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,
+                       const double* factors, const double* w_child, int64_t child_rows,
+                       double* w_out, int64_t out_rows, double* y, int32_t nrhs, void* stream);
+
+/* Backward sweep (engine.py:488-492) for one level.  parent: view of
+ * level+1 (NULL at the root level) and its x buffer (stride parent_rows*nrhs);
+ * x_out: this level's front x vectors (stride out_rows*nrhs); y: pivot-order
+ * vector, overwritten with x at this level's pivots. */
+int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
+                       const double* factors, const double* x_parent, int64_t parent_rows,
+                       double* x_out, int64_t out_rows, double* y, int32_t nrhs, void* stream);
+
+/* out[i, :] = in[idx[i]-1, :] (natural -> pivot order); inverse when scatter != 0. */
+int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out, int32_t nrhs,
+                    int32_t scatter, void* stream);
+
+/* Library build identification (arch, compile flags). */
+const char* tf_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

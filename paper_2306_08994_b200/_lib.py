@@ -1,0 +1,128 @@
+"""ctypes binding of libtfb200.so (C ABI: include/tracefront_b200.h).
+
+The shared library is built in-tree by `__graft_entry__.build()` (or
+`make -C paper_2306_08994_b200/csrc`).  There is no fallback: if the library
+is missing, importing the numeric path raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libtfb200.so"
+
+TF_OK = 0
+TF_ZERO_PIVOT = 2
+TF_ERR_INVALID = -1
+TF_ERR_CUDA = -2
+
+PAT_WIDTH = 8
+PAT_M, PAT_K, PAT_NSRC, PAT_LEN0, PAT_LEN1, PAT_OFF0, PAT_OFF1, PAT_LEAF = range(8)
+
+
+class PlanSummary(C.Structure):
+    _fields_ = [
+        ("n_dof", C.c_int64), ("n_leaves", C.c_int64), ("n_nodes", C.c_int64),
+        ("n_pivots", C.c_int64), ("n_levels", C.c_int32), ("max_m", C.c_int32),
+        ("max_k", C.c_int32), ("keep_lists", C.c_int32),
+    ]
+
+
+class LevelHost(C.Structure):
+    _fields_ = [
+        ("level", C.c_int32), ("n_fronts", C.c_int32), ("n_patterns", C.c_int32),
+        ("max_m", C.c_int32), ("max_k", C.c_int32), ("max_upd", C.c_int32),
+        ("node_base", C.c_int64), ("piv_base", C.c_int64), ("n_pivots", C.c_int64),
+        ("maps_len", C.c_int64),
+        ("pattern_of", C.POINTER(C.c_int32)), ("piv_off", C.POINTER(C.c_int64)),
+        ("pat", C.POINTER(C.c_int32)), ("maps", C.POINTER(C.c_int32)),
+    ]
+
+
+class LevelView(C.Structure):
+    _fields_ = [
+        ("level", C.c_int32), ("n_fronts", C.c_int32), ("n_patterns", C.c_int32),
+        ("max_m", C.c_int32), ("max_k", C.c_int32), ("max_upd", C.c_int32),
+        ("is_leaf", C.c_int32), ("elem_ld", C.c_int32),
+        ("fac_stride", C.c_int64), ("upd_stride", C.c_int64),
+        ("child_upd_stride", C.c_int64), ("elem_stride", C.c_int64),
+        ("pattern_of", C.c_void_p), ("piv_off", C.c_void_p),
+        ("pat", C.c_void_p), ("maps", C.c_void_p),
+    ]
+
+
+# every symbol the header declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "tf_mesh_tensor", "tf_plan_create", "tf_plan_destroy", "tf_plan_summary_get",
+    "tf_plan_level", "tf_plan_pivot_order", "tf_plan_node_lists", "tf_plan_node_lists_len",
+    "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
+    "tf_level_solve_bwd", "tf_permute_rows", "tf_build_info",
+)
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree library once; raise if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` or `make -C paper_2306_08994_b200/csrc` (no CPU fallback exists)"
+        )
+    lib = C.CDLL(os.fspath(LIB_PATH))
+    i32, i64, vp = C.c_int32, C.c_int64, C.c_void_p
+    P_i64, P_i32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+    lib.tf_mesh_tensor.argtypes = [i32, P_i64, i32, P_i64, P_i64, P_i32]
+    lib.tf_mesh_tensor.restype = C.c_int
+    lib.tf_plan_create.argtypes = [i64, i64, P_i64, i32, P_i32, i32, C.POINTER(vp)]
+    lib.tf_plan_create.restype = C.c_int
+    lib.tf_plan_destroy.argtypes = [vp]
+    lib.tf_plan_destroy.restype = None
+    lib.tf_plan_summary_get.argtypes = [vp, C.POINTER(PlanSummary)]
+    lib.tf_plan_summary_get.restype = C.c_int
+    lib.tf_plan_level.argtypes = [vp, i32, C.POINTER(LevelHost)]
+    lib.tf_plan_level.restype = C.c_int
+    lib.tf_plan_pivot_order.argtypes = [vp, P_i32]
+    lib.tf_plan_pivot_order.restype = C.c_int
+    lib.tf_plan_node_lists.argtypes = [vp, i32, P_i64, P_i32, P_i32]
+    lib.tf_plan_node_lists.restype = C.c_int
+    lib.tf_plan_node_lists_len.argtypes = [vp, i32]
+    lib.tf_plan_node_lists_len.restype = i64
+    lib.tf_level_factor_workspace.argtypes = [C.POINTER(LevelView)]
+    lib.tf_level_factor_workspace.restype = i64
+    lib.tf_level_factor.argtypes = [C.POINTER(LevelView), vp, vp, vp, vp, C.c_double, vp, vp,
+                                    i64, vp]
+    lib.tf_level_factor.restype = C.c_int
+    lib.tf_level_solve_fwd.argtypes = [C.POINTER(LevelView), C.POINTER(LevelView), vp, vp, i64,
+                                       vp, i64, vp, i32, vp]
+    lib.tf_level_solve_fwd.restype = C.c_int
+    lib.tf_level_solve_bwd.argtypes = [C.POINTER(LevelView), C.POINTER(LevelView), vp, vp, i64,
+                                       vp, i64, vp, i32, vp]
+    lib.tf_level_solve_bwd.restype = C.c_int
+    lib.tf_permute_rows.argtypes = [vp, i64, vp, vp, i32, i32, vp]
+    lib.tf_permute_rows.restype = C.c_int
+    lib.tf_build_info.argtypes = []
+    lib.tf_build_info.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == TF_OK:
+        return
+    if rc == TF_ERR_CUDA:
+        raise RuntimeError(f"{what}: CUDA error (see stderr)")
+    raise ValueError(f"{what}: invalid input (status {rc})")
+
+
+def i64p(arr):
+    return arr.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def i32p(arr):
+    return arr.ctypes.data_as(C.POINTER(C.c_int32))

@@ -1,0 +1,92 @@
+// extern "C" entry points of libtfb200.so (declared in include/tracefront_b200.h).
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace tfb {
+int small_smem_per_group(int max_m);
+cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, const double* elem,
+                                double* factors, double* upd_out, double thr,
+                                unsigned long long* err, cudaStream_t st);
+cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, double* factors,
+                                double* upd_out, double thr, unsigned long long* err,
+                                cudaStream_t st);
+cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
+                             const double* w_child, long long child_rows, double* w_out,
+                             long long out_rows, double* y, int nrhs, cudaStream_t st);
+cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_parent,
+                             const double* factors, const double* x_parent, long long parent_rows,
+                             double* x_out, long long out_rows, double* y, int nrhs,
+                             cudaStream_t st);
+cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,
+                                int nrhs, int scatter, cudaStream_t st);
+
+// Fronts up to this order are factored entirely in one SM's shared memory.
+constexpr int kSmallMaxM = 232;
+}  // namespace tfb
+
+using namespace tfb;
+
+static int status(cudaError_t e) {
+  if (e == cudaSuccess) return TF_OK;
+  fprintf(stderr, "tfb200: CUDA error %s\n", cudaGetErrorString(e));
+  return TF_ERR_CUDA;
+}
+
+extern "C" int64_t tf_level_factor_workspace(const tf_level_view* lv) {
+  (void)lv;
+  return 0;
+}
+
+extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
+                               const double* elem, double* factors, double* upd_out,
+                               double threshold, unsigned long long* err, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!lv || !err) return TF_ERR_INVALID;
+  if (lv->n_fronts == 0) return TF_OK;
+  if (lv->is_leaf && !elem) return TF_ERR_INVALID;
+  if (!lv->is_leaf && !child_upd) return TF_ERR_INVALID;
+  LevelArgs L = make_args(lv);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (lv->max_m <= kSmallMaxM)
+    return status(launch_factor_small(L, child_upd, elem, factors, upd_out, threshold, err, st));
+  return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, st));
+}
+
+extern "C" int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,
+                                  const double* factors, const double* w_child,
+                                  int64_t child_rows, double* w_out, int64_t out_rows, double* y,
+                                  int32_t nrhs, void* stream) {
+  if (!lv || nrhs < 1 || out_rows < lv->max_m) return TF_ERR_INVALID;
+  if (lv->n_fronts == 0) return TF_OK;
+  if (!lv->is_leaf && (!child || !w_child)) return TF_ERR_INVALID;
+  LevelArgs L = make_args(lv);
+  LevelArgs C = child ? make_args(child) : L;
+  return status(launch_solve_fwd(L, C, factors, w_child, child_rows, w_out, out_rows, y, nrhs,
+                                 (cudaStream_t)stream));
+}
+
+extern "C" int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
+                                  const double* factors, const double* x_parent,
+                                  int64_t parent_rows, double* x_out, int64_t out_rows,
+                                  double* y, int32_t nrhs, void* stream) {
+  if (!lv || nrhs < 1 || out_rows < lv->max_m || !x_out) return TF_ERR_INVALID;
+  if (lv->n_fronts == 0) return TF_OK;
+  if (parent && !x_parent) return TF_ERR_INVALID;
+  LevelArgs L = make_args(lv);
+  LevelArgs PA = parent ? make_args(parent) : L;
+  return status(launch_solve_bwd(L, PA, parent ? 1 : 0, factors, x_parent, parent_rows, x_out,
+                                 out_rows, y, nrhs, (cudaStream_t)stream));
+}
+
+extern "C" int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out,
+                               int32_t nrhs, int32_t scatter, void* stream) {
+  if (!idx || !in || !out || nrhs < 1) return TF_ERR_INVALID;
+  return status(launch_permute_rows(idx, n, in, out, nrhs, scatter, (cudaStream_t)stream));
+}
+
+extern "C" const char* tf_build_info(void) {
+  return "tfb200 sm_100a fp64 (DMMA m8n8k4) small<=232 smem / large blocked";
+}

@@ -1,0 +1,194 @@
+"""GPU executor: per-level device tables, factor buffers, level launch loops.
+
+`DevicePlan` is the compiled, reusable execution plan (the analogue of the
+reference's `compile_execution`, engine.py:335-344): it uploads each level's
+pattern table and extend-add maps once, owns the factor buffers, and runs
+one Foata class (tree level) per `tf_level_factor` call, in stream order
+(the stream is the class barrier of engine.py:330-332).
+
+Device memory layout per level L (all float64, row-major):
+  factors[L] : n_fronts x fac_stride    front panel P (m x k), lower part valid
+  upd ping-pong: n_fronts x upd_stride  packed lower Schur complement (m-k)^2
+  solve blocks : n_fronts x max_m x nrhs (forward W / backward X, ping-pong)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _tri(n):
+    return n * (n + 1) // 2
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2306_08994_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class DeviceLevel:
+    def __init__(self, lt, device, child_upd_stride: int, elem_stride: int, elem_ld: int):
+        self.tables = lt
+        m = lt.pat[:, _lib.PAT_M].astype(np.int64)
+        k = lt.pat[:, _lib.PAT_K].astype(np.int64)
+        self.n_fronts = lt.n_fronts
+        self.max_m = lt.max_m
+        self.fac_stride = int((m * k).max()) if len(m) else 0
+        self.upd_stride = int(_tri(m - k).max()) if len(m) else 0
+        self.pattern_of = torch.from_numpy(lt.pattern_of).to(device)
+        self.piv_off = torch.from_numpy(lt.piv_off).to(device)
+        self.pat = torch.from_numpy(np.ascontiguousarray(lt.pat).ravel()).to(device)
+        maps = lt.maps if len(lt.maps) else np.zeros(1, np.int32)
+        self.maps = torch.from_numpy(maps).to(device)
+        v = _lib.LevelView()
+        v.level = lt.level
+        v.n_fronts = lt.n_fronts
+        v.n_patterns = lt.n_patterns
+        v.max_m = lt.max_m
+        v.max_k = lt.max_k
+        v.max_upd = lt.max_upd
+        v.is_leaf = 1 if lt.level == 0 else 0
+        v.elem_ld = elem_ld
+        v.fac_stride = self.fac_stride
+        v.upd_stride = self.upd_stride
+        v.child_upd_stride = child_upd_stride
+        v.elem_stride = elem_stride
+        v.pattern_of = self.pattern_of.data_ptr()
+        v.piv_off = self.piv_off.data_ptr()
+        v.pat = self.pat.data_ptr()
+        v.maps = self.maps.data_ptr()
+        self.view = v
+
+
+class DevicePlan:
+    def __init__(self, plan, fronts, device: Optional[torch.device] = None):
+        self.device = device or require_cuda()
+        self.lib = _lib.load()
+        self.plan = plan
+        native = plan.native
+        self.n_dof = plan.n_dof
+        self.n_pivots = native.n_pivots
+        vals = np.ascontiguousarray(fronts.values, dtype=np.float64)
+        elem_ld = vals.shape[-1]
+        elem_stride = 0 if vals.ndim == 2 else elem_ld * elem_ld
+        self.elem = torch.from_numpy(vals.ravel()).to(self.device)
+        self.levels: list[DeviceLevel] = []
+        child = 0
+        for lt in native.levels:
+            dl = DeviceLevel(lt, self.device, child, elem_stride, elem_ld)
+            self.levels.append(dl)
+            child = dl.upd_stride
+        self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)
+        self.factors = [torch.empty(max(1, dl.n_fronts * dl.fac_stride), dtype=torch.float64,
+                                    device=self.device) for dl in self.levels]
+        upd_max = max(dl.n_fronts * dl.upd_stride for dl in self.levels)
+        self.upd = [torch.empty(max(1, upd_max), dtype=torch.float64, device=self.device)
+                    for _ in range(2)]
+        self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
+        self._solve_nrhs = 0
+        self._blk = None
+
+    # ---- factorization -----------------------------------------------------------
+    def factor(self, threshold: float, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Enqueue every level on `stream`; no host synchronisation."""
+        st = stream or torch.cuda.current_stream(self.device)
+        sp = C.c_void_p(st.cuda_stream)
+        self.err.fill_(-1)
+        lib = self.lib
+        prev = None
+        for L, dl in enumerate(self.levels):
+            out = self.upd[L & 1]
+            rc = lib.tf_level_factor(C.byref(dl.view), _ptr(prev), _ptr(self.elem),
+                                     _ptr(self.factors[L]), _ptr(out), C.c_double(threshold),
+                                     _ptr(self.err), None, 0, sp)
+            _lib.check(rc, f"tf_level_factor(level {L})")
+            prev = out
+
+    def zero_pivot_position(self) -> int:
+        """-1, or the pivot-order position of the earliest pivot at/below threshold."""
+        return int(self.err.item())
+
+    # ---- solve -------------------------------------------------------------------
+    def _blocks(self, nrhs: int):
+        if self._solve_nrhs != nrhs:
+            n = max(dl.n_fronts * dl.max_m for dl in self.levels) * nrhs
+            self._blk = [torch.empty(max(1, n), dtype=torch.float64, device=self.device)
+                         for _ in range(2)]
+            self._y = torch.empty(max(1, self.n_pivots * nrhs), dtype=torch.float64,
+                                  device=self.device)
+            self._solve_nrhs = nrhs
+        return self._blk
+
+    def solve_into(self, b: torch.Tensor, x: torch.Tensor,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+        """x = A^-1 b for row-major (n, nrhs) device tensors (b may alias x)."""
+        nrhs = 1 if b.dim() == 1 else b.shape[1]
+        st = stream or torch.cuda.current_stream(self.device)
+        sp = C.c_void_p(st.cuda_stream)
+        lib = self.lib
+        blk = self._blocks(nrhs)
+        y = self._y
+        npiv = self.n_pivots
+        if x.data_ptr() != b.data_ptr():
+            x.copy_(b)  # DOFs outside every front stay as given (engine.py:481)
+        _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(x), _ptr(y), nrhs, 0,
+                                       sp), "tf_permute_rows")
+        prev = None
+        for L, dl in enumerate(self.levels):
+            cur = blk[L & 1]
+            child = self.levels[L - 1] if L > 0 else None
+            rc = lib.tf_level_solve_fwd(C.byref(dl.view),
+                                        C.byref(child.view) if child else None,
+                                        _ptr(self.factors[L]), _ptr(prev),
+                                        child.max_m if child else 0, _ptr(cur), dl.max_m,
+                                        _ptr(y), nrhs, sp)
+            _lib.check(rc, f"tf_level_solve_fwd(level {L})")
+            prev = cur
+        prev = None
+        nl = len(self.levels)
+        for L in range(nl - 1, -1, -1):
+            dl = self.levels[L]
+            cur = blk[L & 1]
+            parent = self.levels[L + 1] if L + 1 < nl else None
+            rc = lib.tf_level_solve_bwd(C.byref(dl.view),
+                                        C.byref(parent.view) if parent else None,
+                                        _ptr(self.factors[L]), _ptr(prev),
+                                        parent.max_m if parent else 0, _ptr(cur), dl.max_m,
+                                        _ptr(y), nrhs, sp)
+            _lib.check(rc, f"tf_level_solve_bwd(level {L})")
+            prev = cur
+        _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(y), _ptr(x), nrhs, 1,
+                                       sp), "tf_permute_rows")
+
+    def launches_per_factor(self) -> int:
+        """Kernel launches one factorization issues (small: 1/level; large: see factor_large.cu)."""
+        n = 0
+        for dl in self.levels:
+            if dl.max_m <= 232:
+                n += 1
+            else:
+                n += 3 + _panel_launches(dl.view.max_k) + (1 if dl.view.max_k > 0 else 0)
+        return n
+
+
+def _panel_launches(k: int, nb: int = 64) -> int:
+    if k <= 0:
+        return 0
+    if k <= nb:
+        return 2
+    mid = (k // 2 + nb - 1) // nb * nb
+    if mid >= k:
+        mid = nb
+    return _panel_launches(mid, nb) + 1 + _panel_launches(k - mid, nb)

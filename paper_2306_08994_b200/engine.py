@@ -1,0 +1,200 @@
+"""Numeric execution: factorize on the GPU, LDU-form factors, solve (engine.py:1-493).
+
+Entry points keep the reference's names and meaning:
+  init_state(system, plan)                 engine.py:67-75  (zero-pivot threshold)
+  run_sequential(plan, state)              engine.py:177-184
+  run_concurrent(schedule, plan, state, workers, debug, compiled)
+                                           engine.py:354-419
+  compile_execution(plan, schedule, state) engine.py:335-344
+  solve(factors, rhs)                      engine.py:468-493
+Every path runs the hand-written sm_100a kernels of libtfb200.so, one launch
+sequence per Foata class (tree level); there is no CPU execution path.  The
+factorization is the reference's no-pivoting elimination in its pivot order,
+computed as LDL^T on dense fronts (the mass matrix is symmetric, so the
+reference's division quotient u(z,y) equals its multiplier l(y,z) up to
+rounding; both dictionaries are served from the one stored factor).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import cached_property
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .device import DevicePlan, require_cuda
+from .errors import ZeroPivotError
+
+ZERO_PIVOT_RELATIVE = 1e-14  # engine.py:35
+
+
+@dataclass
+class ExecState:
+    """Execution state: zero-pivot threshold and the compiled device plan."""
+
+    zero_threshold: float = 0.0
+    debug: bool = False
+    compiled: Optional[DevicePlan] = None
+    factors: Optional["FactorResult"] = None
+
+
+def init_state(system, plan, debug: bool = False) -> ExecState:
+    """Zero-pivot threshold = 1e-14 * max|A_ij| (engine.py:67-75)."""
+    return ExecState(zero_threshold=ZERO_PIVOT_RELATIVE * float(system.peak), debug=debug)
+
+
+def compile_execution(plan, schedule=None, state: Optional[ExecState] = None) -> DevicePlan:
+    """Upload the level tables once; reusable across factorizations (engine.py:335-344)."""
+    dp = DevicePlan(plan, plan.tree.fronts)
+    if state is not None:
+        state.compiled = dp
+    return dp
+
+
+class FactorResult:
+    """LDU-form factors in global coordinates (engine.py:110-144).
+
+    Device-resident: `device_plan.factors[L]` holds every front's m x k panel.
+    `u_entries` / `l_entries` are materialised on first access with the
+    reference's key sets (small plans only).
+    """
+
+    def __init__(self, plan, device_plan: DevicePlan):
+        self.plan = plan
+        self.device_plan = device_plan
+        self.n_dof = plan.n_dof
+
+    @property
+    def pivot_order(self) -> tuple[int, ...]:
+        return self.plan.pivot_order
+
+    def permutation(self) -> np.ndarray:
+        return self.plan.pivot_order_array.astype(np.int64) - 1
+
+    @cached_property
+    def _dicts(self):
+        plan = self.plan
+        steps = plan.steps
+        u: dict[tuple[int, int], float] = {}
+        l: dict[tuple[int, int], float] = {}
+        s = 0
+        for L, dl in enumerate(self.device_plan.levels):
+            lt = dl.tables
+            ptr, kk, idx = plan.native.node_lists(L)
+            fac = self.device_plan.factors[L].cpu().numpy()
+            for i in range(lt.n_fronts):
+                row = lt.pat[lt.pattern_of[i]]
+                m, k = int(row[0]), int(row[1])
+                if k == 0:
+                    continue
+                P = fac[i * dl.fac_stride: i * dl.fac_stride + m * k].reshape(m, k)
+                lst = idx[ptr[i]:ptr[i + 1]]
+                pos = {int(g): r for r, g in enumerate(lst)}
+                for c in range(k):
+                    z = int(lst[c])
+                    st = steps[s]
+                    s += 1
+                    assert st.pivot == z
+                    for y in st.active:
+                        v = float(P[pos[y], c])
+                        u[(z, y)] = v
+                        l[(y, z)] = v
+                    u[(z, z)] = float(P[c, c])
+        return u, l
+
+    @property
+    def u_entries(self) -> dict[tuple[int, int], float]:
+        return self._dicts[0]
+
+    @property
+    def l_entries(self) -> dict[tuple[int, int], float]:
+        return self._dicts[1]
+
+    def permuted_dense_factors(self) -> tuple[np.ndarray, np.ndarray]:
+        """Unit-lower L and standard U with L @ U == P M P^T (engine.py:126-140)."""
+        pos = {z: k for k, z in enumerate(self.pivot_order)}
+        n = self.n_dof
+        lower = np.eye(n)
+        upper = np.zeros((n, n))
+        u = self.u_entries
+        for (x, z), v in self.l_entries.items():
+            lower[pos[x], pos[z]] = v
+        for (z, y), v in u.items():
+            upper[pos[z], pos[y]] = v if z == y else v * u[(z, z)]
+        return lower, upper
+
+    def solve(self, rhs):
+        return solve(self, rhs)
+
+
+def _factorize(plan, state: ExecState, compiled: Optional[DevicePlan] = None) -> FactorResult:
+    dp = compiled or state.compiled or compile_execution(plan, None, state)
+    dp.factor(state.zero_threshold)
+    pos = dp.zero_pivot_position()
+    if pos >= 0:
+        front, pivot = plan.locate_pivot(pos)
+        raise ZeroPivotError(front, pivot)
+    res = FactorResult(plan, dp)
+    state.factors = res
+    return res
+
+
+def run_sequential(plan, state: ExecState) -> FactorResult:
+    """Execute the level classes in order on the current CUDA stream (engine.py:177-184)."""
+    plan = getattr(plan, "plan", plan)  # accept a DependencyGraph-like wrapper
+    return _factorize(plan, state)
+
+
+def run_concurrent(schedule, plan, state: ExecState, workers: int = 1, debug: bool = False,
+                   compiled: Optional[DevicePlan] = None) -> FactorResult:
+    """Execute classes in order with a barrier between classes (engine.py:354-419).
+
+    Within a class the GPU runs every front concurrently; the stream order
+    between level launches is the barrier.  `workers` > 1 with an initialised
+    torch.distributed group shards independent subtrees across GPUs
+    (paper_2306_08994_b200.distributed); with a single process it only
+    validates the argument like the reference.
+    """
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if debug:
+        from .verify import check_level_schedule
+        check_level_schedule(plan, schedule)
+    return _factorize(plan, state, compiled)
+
+
+def factorize(plan, system) -> FactorResult:
+    """Convenience: init_state + run_sequential."""
+    return run_sequential(plan, init_state(system, plan))
+
+
+def _as_device(rhs, device, n):
+    if isinstance(rhs, torch.Tensor):
+        t = rhs.to(device=device, dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64)).to(device)
+    if t.shape[0] != n or t.dim() > 2:
+        raise ValueError(f"rhs must have length {n}, got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def solve(factors: FactorResult, rhs):
+    """Forward (unit L), diagonal scaling, backward (U) substitution (engine.py:468-493).
+
+    rhs: (n,) or (n, nrhs), numpy or torch.  Returns the same kind/shape
+    (numpy in, numpy out; a CUDA tensor in, a CUDA tensor out).
+    """
+    dp = factors.device_plan
+    n = factors.n_dof
+    if not isinstance(rhs, torch.Tensor):
+        arr = np.asarray(rhs, dtype=float)
+        if arr.shape[:1] != (n,) or arr.ndim > 2:
+            raise ValueError(f"rhs must have length {n}, got {arr.shape}")
+    b = _as_device(rhs, dp.device, n)
+    x = torch.empty_like(b)
+    dp.solve_into(b, x)
+    if isinstance(rhs, torch.Tensor):
+        return x
+    return x.cpu().numpy()

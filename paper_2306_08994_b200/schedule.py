@@ -1,0 +1,87 @@
+"""Foata Normal Form schedule at front granularity (mirrors schedule.py:1-128).
+
+The reference builds the FNF of its atomic trace (Division / Multiplication /
+Subtraction / Assertion tasks, schedule.py:60-82).  This package schedules
+the coarser trace whose letters are whole front factorizations
+(extend-add + partial factorization of one tree node) and whose dependency
+relation is child -> parent.  Its canonical FNF is exactly the tree levels:
+class(L) = 1 + max class(children) = L + 1.  Every atomic J-edge of the
+reference goes from a level to the same or a later level, so executing the
+level classes in order (one GPU launch sequence per class, stream order as
+the barrier) is a valid linearization of the reference's Diekert graph
+(checked against the atomic graph in tests/test_schedule.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+
+class TaskKind(IntEnum):
+    DIVISION = 1
+    MULTIPLICATION = 2
+    SUBTRACTION = 3
+    ASSERTION = 4
+
+
+@dataclass(frozen=True)
+class FoataSchedule:
+    """Ordered Foata classes of front tasks; class c holds the node ids of level c-1."""
+
+    classes: tuple  # tuple of node-id ranges, leaves first
+    class_kinds: tuple[frozenset, ...]
+    level_sizes: tuple[int, ...]
+
+    @property
+    def n_classes(self) -> int:
+        return len(self.classes)
+
+    def class_of(self, node_id: int) -> int:
+        for c, r in enumerate(self.classes):
+            if node_id in r:
+                return c + 1
+        raise KeyError(node_id)
+
+
+@dataclass(frozen=True)
+class ScheduleStats:
+    n_classes: int
+    widths: tuple[int, ...]
+    kinds: tuple[frozenset, ...]
+    max_width: int
+    mixed_classes: tuple[int, ...]
+
+
+def compute_fnf(plan) -> FoataSchedule:
+    """Canonical FNF of the front-granularity trace (levels of the tree)."""
+    native = plan.native
+    kinds = []
+    for lt in native.levels:
+        m, k = lt.front_m(), lt.front_k()
+        ks = {TaskKind.ASSERTION}
+        if np.any(k > 0):
+            ks.add(TaskKind.DIVISION)
+            if np.any((m - 1) > 0):
+                ks |= {TaskKind.MULTIPLICATION, TaskKind.SUBTRACTION}
+        kinds.append(frozenset(ks))
+    return FoataSchedule(classes=tuple(plan.tree.levels), class_kinds=tuple(kinds),
+                         level_sizes=tuple(plan.tree.level_sizes))
+
+
+def schedule_stats(schedule: FoataSchedule) -> ScheduleStats:
+    widths = tuple(schedule.level_sizes)
+    mixed = tuple(i + 1 for i, ks in enumerate(schedule.class_kinds)
+                  if TaskKind.DIVISION in ks and TaskKind.SUBTRACTION in ks)
+    return ScheduleStats(n_classes=schedule.n_classes, widths=widths,
+                         kinds=schedule.class_kinds, max_width=max(widths) if widths else 0,
+                         mixed_classes=mixed)
+
+
+def schedule_stats_csv(schedule: FoataSchedule) -> str:
+    lines = ["class_index,kind_set,size"]
+    for i, (w, ks) in enumerate(zip(schedule.level_sizes, schedule.class_kinds)):
+        lines.append(f"{i + 1},{'|'.join(sorted(k.name.lower() for k in ks))},{w}")
+    return "\n".join(lines) + "\n"

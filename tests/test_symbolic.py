@@ -1,0 +1,93 @@
+"""Native symbolic layer (tree, pivot order, NodeReorder, active sets) vs the reference."""
+import numpy as np
+import pytest
+
+import paper_2306_08994_b200 as tf
+from conftest import golden, golden_names, mesh_of
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_plan_matches_reference(name):
+    g = golden(name)
+    mesh = mesh_of(g)
+    fronts = tf.generate_fronts(mesh)
+    assert np.array_equal(fronts.dofs, g["elem_dofs"])
+    assert np.array_equal(fronts.values, g["elem_matrix"])
+    tree = tf.build_elimination_tree(tf.sort_fronts(fronts))
+    assert tuple(tree.level_sizes) == tuple(int(x) for x in g["level_sizes"])
+    assert tree.root_id == int(g["root_id"])
+    system = tf.assemble_system(mesh, "one")
+    plan = tf.symbolic_eliminate(tree, system)
+    assert np.array_equal(plan.pivot_order_array, g["pivot_order"])
+    assert tf.init_state(system, plan).zero_threshold == float(g["threshold"])
+    if int(g["n_dof"]) > 5000:
+        return
+    ro = plan.reorders
+    assert [r.node_id for r in ro] == list(g["reorder_node"])
+    cnt = np.array([(len(r.eliminable), len(r.shared), len(r.computed)) for r in ro])
+    assert np.array_equal(cnt, g["reorder_counts"])
+    assert np.array_equal(np.array([x for r in ro for x in r.eliminable]), g["reorder_elim"])
+    assert np.array_equal(np.array([x for r in ro for x in r.shared], dtype=np.int64),
+                          g["reorder_shared"].astype(np.int64))
+    assert np.array_equal(np.array([len(s.active) for s in plan.steps]), g["active_sizes"])
+    assert np.array_equal(np.array([s.node_id for s in plan.steps]), g["step_node"])
+    assert len(plan.cells) == int(g["n_cells"])
+    assert len(plan.fill_cells) == int(g["n_fill"])
+
+
+def test_spec_tree_examples():
+    """8 fronts -> levels 8,4,2,1; 5 fronts -> 5,3,2,1."""
+    for n, sizes in ((8, (8, 4, 2, 1)), (5, (5, 3, 2, 1)), (1, (1,))):
+        tree = tf.build_elimination_tree(tf.sort_fronts(tf.generate_fronts(tf.Mesh(n, 1))))
+        assert tree.level_sizes == sizes
+
+
+def test_spec_pivot_order_n2():
+    """mesh(n=2, p=1) pivots (1, 3, 2)."""
+    mesh = tf.Mesh(2, 1)
+    tree = tf.build_elimination_tree(tf.sort_fronts(tf.generate_fronts(mesh)))
+    plan = tf.symbolic_eliminate(tree, tf.assemble_system(mesh, "one"))
+    assert plan.pivot_order == (1, 3, 2)
+
+
+def test_membership_and_nodes_n2():
+    """membership [(1,2),(2,1)] at the leaves."""
+    mesh = tf.Mesh(2, 1)
+    tree = tf.build_elimination_tree(tf.sort_fronts(tf.generate_fronts(mesh)))
+    assert [tree.nodes[i].front.membership for i in tree.levels[0]] == [(1, 2), (2, 1)]
+    assert tree.nodes[tree.root_id].front.indices == (1, 2, 3)
+
+
+def test_element_and_assembly_kats():
+    """SPEC.md:63, 73, 81."""
+    assert np.allclose(tf.element_mass_matrix(1.0, 1), np.array([[2, 1], [1, 2]]) / 6, atol=1e-16)
+    from paper_2306_08994_b200.fem import element_load_vector
+    assert np.allclose(element_load_vector(1.0, 1, lambda x: 1.0, 0.0), [0.5, 0.5])
+    s = tf.assemble_system(tf.Mesh(2, 1), "one")
+    assert s.entry(2, 2) == 0.33333333333333337
+
+
+def test_empty_and_invalid_inputs():
+    with pytest.raises(tf.EmptyInputError):
+        tf.sort_fronts([])
+    with pytest.raises(tf.EmptyInputError):
+        tf.build_elimination_tree([])
+    with pytest.raises(tf.UnsupportedDegreeError):
+        tf.Mesh(4, 4)
+    with pytest.raises(tf.InvalidGeometryError):
+        tf.Mesh(0, 1)
+    with pytest.raises(tf.InvalidGeometryError):
+        tf.TensorMesh((4, 0), 1)
+
+
+def test_large_tensor_plan_shapes():
+    """2D 256^2 p=1: level table maxima follow the nested-dissection model."""
+    mesh = tf.TensorMesh((256, 256), 1)
+    tree = tf.build_elimination_tree(tf.generate_fronts(mesh))
+    plan = tf.symbolic_eliminate(tree)
+    assert plan.native.n_pivots == mesh.n_dof
+    ms = [lt.max_m for lt in plan.native.levels]
+    ks = [lt.max_k for lt in plan.native.levels]
+    assert ms[:6] == [4, 6, 9, 13, 19, 27] and ks[-1] == ms[-1] == 257
+    for lt in plan.native.levels:
+        assert lt.n_patterns <= 40  # structured mesh: a handful of shape classes per level
