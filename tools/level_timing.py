@@ -1,0 +1,63 @@
+"""Per-level timing of the GPU factorization + solve (CUDA events), for profiling runs."""
+import argparse, ctypes as C, json, sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np, torch
+import paper_2306_08994_b200 as tf
+from paper_2306_08994_b200 import _lib
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--shape", default="1024,1024")
+ap.add_argument("--degree", type=int, default=1)
+ap.add_argument("--nrhs", type=int, default=1)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+shape = tuple(int(x) for x in a.shape.split(","))
+t0 = time.time()
+mesh = tf.TensorMesh(shape, a.degree)
+fronts = tf.generate_fronts(mesh)
+tree = tf.build_elimination_tree(tf.sort_fronts(fronts), n_dof=mesh.n_dof)
+system = tf.assemble_system(mesh, "one")
+plan = tf.symbolic_eliminate(tree, system)
+state = tf.init_state(system, plan)
+dp = tf.compile_execution(plan, None, state)
+print(f"plan {time.time()-t0:.1f}s n_dof={mesh.n_dof}", flush=True)
+stats = plan.level_stats()
+lib = dp.lib
+def run_levels():
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(dp.levels) + 1)]
+    dp.err.fill_(-1)
+    prev = None
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ev[0].record()
+    for L, dl in enumerate(dp.levels):
+        out = dp.upd[L & 1]
+        rc = lib.tf_level_factor(C.byref(dl.view), None if prev is None else C.c_void_p(prev.data_ptr()),
+                                 C.c_void_p(dp.elem.data_ptr()), C.c_void_p(dp.factors[L].data_ptr()),
+                                 C.c_void_p(out.data_ptr()), C.c_double(state.zero_threshold),
+                                 C.c_void_p(dp.err.data_ptr()), None, 0, sp)
+        assert rc == 0
+        prev = out
+        ev[L + 1].record()
+    torch.cuda.synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) for i in range(len(dp.levels))]
+for r in range(a.reps):
+    times = run_levels()
+assert dp.zero_pivot_position() == -1
+tot = sum(times)
+print(f"factor total {tot:.3f} ms")
+for L, (t, s) in enumerate(zip(times, stats)):
+    gfs = s["ldl_flops"] / t / 1e9 if t > 0 else 0
+    gbs = s["bytes"] / t / 1e6 if t > 0 else 0
+    print(f"L{L:2d} fronts={s['fronts']:9d} m={s['max_m']:5d} k={s['max_k']:5d} t={t:8.3f}ms "
+          f"{gfs/1e3:7.2f} TF/s {gbs:8.1f} GB/s")
+b = torch.randn(mesh.n_dof, a.nrhs, dtype=torch.float64, device="cuda")
+x = torch.empty_like(b)
+for r in range(a.reps):
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); dp.solve_into(b, x); e1.record(); torch.cuda.synchronize()
+ts = e0.elapsed_time(e1)
+print(f"solve nrhs={a.nrhs} {ts:.3f} ms")
+r = torch.from_numpy(system.matvec(x.cpu().numpy())).cuda() - b
+print("rel residual", (r.abs().max() / b.abs().max()).item())
+print(json.dumps({"factor_ms": tot, "solve_ms": ts, "dof_per_s": mesh.n_dof / (tot + ts) * 1e3}))
