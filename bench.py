@@ -264,7 +264,7 @@ def run_ours(args, cfg):
     t_s = level_ms[L] / 1e3
     ridge = FP64_PEAK_TFLOPS * 1e12 / (hbm * 1e9)
     intensity = st["ldl_flops"] / max(st["bytes"], 1.0)
-    small = dp.levels[L].max_m <= 232
+    small = dp.levels[L].max_m <= 232  # default tf_set_small_max_m
     kname = "factor_small_kernel" if small else "large level sequence (DMMA update/diag/trsm)"
     if intensity < ridge:
         roof = {"bound": "hbm", "achieved": st["bytes"] / t_s / 1e9, "peak": hbm, "unit": "GB/s"}
@@ -278,7 +278,7 @@ def run_ours(args, cfg):
     roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
                            "measured cuBLAS DGEMM 35.47 TF/s (profiles/r01_dgemm_cublas_peak.log)")
 
-    launches = dp.launches_per_factor() + 2 + 2 * nl
+    launches = dp.launches_per_factor() + dp.launches_per_solve(nrhs)
     total_ldl = sum(s["ldl_flops"] for s in stats)
     total_bytes = sum(s["bytes"] for s in stats)
     line = {

@@ -30,7 +30,7 @@ extern "C" {
 #define TF_ERR_STRAY (-3) /* pivot couples outside its front (tasks.py:136-140) */
 
 /* Pattern table row layout (int32 x TF_PAT_WIDTH per pattern). */
-#define TF_PAT_WIDTH 8
+#define TF_PAT_WIDTH 12
 #define TF_PAT_M 0      /* front order (non-eliminated indices) */
 #define TF_PAT_K 1      /* pivots eliminated in this front */
 #define TF_PAT_NSRC 2   /* 1 (element or carry child) or 2 children */
@@ -39,6 +39,10 @@ extern "C" {
 #define TF_PAT_OFF0 5   /* offset of source-0 map in the maps array */
 #define TF_PAT_OFF1 6
 #define TF_PAT_LEAF 7   /* 1 when source 0 is an element matrix */
+#define TF_PAT_IOFF 8   /* inverse maps: front position -> source position (-1 if none);
+                           source 0 at maps[IOFF, IOFF+m), source 1 at [IOFF+m, IOFF+2m) */
+#define TF_PAT_KP 9     /* panel leading dimension: k rounded up to a multiple of 4 */
+#define TF_PAT_FAC 10   /* doubles of the front's factor slot: m*kp (panel) + kp (diag) */
 
 /* ------------------------------------------------------------------ mesh */
 
@@ -163,6 +167,15 @@ int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
 /* out[i, :] = in[idx[i]-1, :] (natural -> pivot order); inverse when scatter != 0. */
 int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out, int32_t nrhs,
                     int32_t scatter, void* stream);
+
+/* Kernel launches one call issues for this level: phase 0 tf_level_factor,
+ * 1 tf_level_solve_fwd, 2 tf_level_solve_bwd. */
+int32_t tf_level_launch_count(const tf_level_view* lv, int32_t nrhs, int32_t phase);
+
+/* Front order up to which a level runs the shared-memory kernels (default and
+ * maximum 232); smaller values route levels through the blocked large-front
+ * kernels (a test and tuning knob).  Returns the previous value. */
+int32_t tf_set_small_max_m(int32_t m);
 
 /* Library build identification (arch, compile flags). */
 const char* tf_build_info(void);

@@ -18,8 +18,9 @@ TF_ZERO_PIVOT = 2
 TF_ERR_INVALID = -1
 TF_ERR_CUDA = -2
 
-PAT_WIDTH = 8
-PAT_M, PAT_K, PAT_NSRC, PAT_LEN0, PAT_LEN1, PAT_OFF0, PAT_OFF1, PAT_LEAF = range(8)
+PAT_WIDTH = 12
+(PAT_M, PAT_K, PAT_NSRC, PAT_LEN0, PAT_LEN1, PAT_OFF0, PAT_OFF1, PAT_LEAF, PAT_IOFF, PAT_KP,
+ PAT_FAC) = range(11)
 
 
 class PlanSummary(C.Structure):
@@ -58,7 +59,8 @@ EXPORTS = (
     "tf_mesh_tensor", "tf_plan_create", "tf_plan_destroy", "tf_plan_summary_get",
     "tf_plan_level", "tf_plan_pivot_order", "tf_plan_node_lists", "tf_plan_node_lists_len",
     "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
-    "tf_level_solve_bwd", "tf_permute_rows", "tf_build_info",
+    "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
+    "tf_build_info",
 )
 
 _lib = None
@@ -106,6 +108,10 @@ def load() -> C.CDLL:
     lib.tf_level_solve_bwd.restype = C.c_int
     lib.tf_permute_rows.argtypes = [vp, i64, vp, vp, i32, i32, vp]
     lib.tf_permute_rows.restype = C.c_int
+    lib.tf_level_launch_count.argtypes = [C.POINTER(LevelView), i32, i32]
+    lib.tf_level_launch_count.restype = i32
+    lib.tf_set_small_max_m.argtypes = [i32]
+    lib.tf_set_small_max_m.restype = i32
     lib.tf_build_info.argtypes = []
     lib.tf_build_info.restype = C.c_char_p
     _lib = lib

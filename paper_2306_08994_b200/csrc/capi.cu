@@ -20,9 +20,9 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
                              cudaStream_t st);
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,
                                 int nrhs, int scatter, cudaStream_t st);
-
-// Fronts up to this order are factored entirely in one SM's shared memory.
-constexpr int kSmallMaxM = 232;
+int large_panel_launches(int max_k);
+int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
+int g_small_max_m = kSmallMaxM;
 }  // namespace tfb
 
 using namespace tfb;
@@ -50,7 +50,7 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
   if (!lv->is_leaf && !child_upd) return TF_ERR_INVALID;
   LevelArgs L = make_args(lv);
   cudaStream_t st = (cudaStream_t)stream;
-  if (lv->max_m <= kSmallMaxM)
+  if (lv->is_leaf || lv->max_m <= g_small_max_m)  // element fronts are always small
     return status(launch_factor_small(L, child_upd, elem, factors, upd_out, threshold, err, st));
   return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, st));
 }
@@ -85,6 +85,22 @@ extern "C" int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, 
                                int32_t nrhs, int32_t scatter, void* stream) {
   if (!idx || !in || !out || nrhs < 1) return TF_ERR_INVALID;
   return status(launch_permute_rows(idx, n, in, out, nrhs, scatter, (cudaStream_t)stream));
+}
+
+extern "C" int32_t tf_level_launch_count(const tf_level_view* lv, int32_t nrhs, int32_t phase) {
+  if (!lv || lv->n_fronts == 0) return 0;
+  LevelArgs L = make_args(lv);
+  if (phase == 0) {
+    if (lv->is_leaf || lv->max_m <= g_small_max_m) return 1;
+    return 3 + large_panel_launches(lv->max_k) + (lv->max_k > 0 && lv->max_upd > 0 ? 1 : 0);
+  }
+  return solve_launches(L, nrhs, phase == 1);
+}
+
+extern "C" int32_t tf_set_small_max_m(int32_t m) {
+  const int old = g_small_max_m;
+  if (m >= 1 && m <= kSmallMaxM) g_small_max_m = m;
+  return old;
 }
 
 extern "C" const char* tf_build_info(void) {

@@ -3,9 +3,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "tracefront_b200.h"
 
 namespace tfb {
+
+// Fronts up to this order are factored entirely in one SM's shared memory.
+constexpr int kSmallMaxM = 232;
+// Runtime threshold (<= kSmallMaxM) between the shared-memory and the blocked
+// large-front paths; lowered by tests to drive the large path on small meshes.
+extern int g_small_max_m;
 
 // Kernel-side copy of tf_level_view (passed by value).
 struct LevelArgs {
@@ -44,23 +52,54 @@ inline LevelArgs make_args(const tf_level_view* v) {
   return a;
 }
 
+// Per-front view of the pattern row.
+struct Shape {
+  int m, k, kp, nsrc, len0, len1, off0, off1, ioff;
+};
+
+__device__ __forceinline__ Shape front_shape(const LevelArgs& L, long long f) {
+  const int* P = L.pat + (size_t)L.pattern_of[f] * TF_PAT_WIDTH;
+  Shape s;
+  s.m = P[TF_PAT_M];
+  s.k = P[TF_PAT_K];
+  s.kp = P[TF_PAT_KP];
+  s.nsrc = P[TF_PAT_NSRC];
+  s.len0 = P[TF_PAT_LEN0];
+  s.len1 = P[TF_PAT_LEN1];
+  s.off0 = P[TF_PAT_OFF0];
+  s.off1 = P[TF_PAT_OFF1];
+  s.ioff = P[TF_PAT_IOFF];
+  return s;
+}
+
 // Packed lower-triangular row-major offset of (r, c), c <= r.
 __host__ __device__ __forceinline__ long long tri(long long r, long long c) {
   return r * (r + 1) / 2 + c;
 }
 
-// Inverse of tri(): row of packed index e.
+// Row of packed index e (exact for any e < 2^50).
 __device__ __forceinline__ int tri_row(long long e) {
-  int r = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+  int r;
+  if (e < (1LL << 22)) {
+    r = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  } else {
+    r = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+  }
   while ((long long)r * (r + 1) / 2 > e) r--;
   while ((long long)(r + 1) * (r + 2) / 2 <= e) r++;
   return r;
 }
 
-// Barrier over a group of G threads (G = 32: warp; else named barrier id).
+// Barrier over a group of G threads: G < 32 lanes of one warp (mask), a
+// warp, or a named barrier covering G threads (id >= 1).
 template <int G>
 __device__ __forceinline__ void group_sync(int bar_id) {
-  if constexpr (G == 32) {
+  if constexpr (G < 32) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned base = lane & ~(unsigned)(G - 1);
+    const unsigned mask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << base;
+    __syncwarp(mask);
+  } else if constexpr (G == 32) {
     __syncwarp();
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(G) : "memory");
@@ -70,6 +109,27 @@ __device__ __forceinline__ void group_sync(int bar_id) {
 __device__ __forceinline__ void record_zero_pivot(unsigned long long* err,
                                                   unsigned long long pos) {
   atomicMin(err, pos);
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 }  // namespace tfb

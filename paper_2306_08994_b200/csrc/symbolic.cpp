@@ -332,8 +332,17 @@ extern "C" int tf_plan_create(int64_t n_dof, int64_t n_elem, const int64_t* elem
         found = lv.n_patterns++;
         int32_t off0 = (int32_t)lv.maps.size();
         lv.maps.insert(lv.maps.end(), fmap.begin() + mptr[i], fmap.begin() + mptr[i + 1]);
+        // inverse (gather) maps: front position -> source position, -1 when absent
+        int32_t ioff = (int32_t)lv.maps.size();
+        lv.maps.insert(lv.maps.end(), (size_t)fm[i] * nsrc, -1);
+        for (int c = 0; c < nsrc; c++) {
+          const int32_t* fwd = fmap.data() + mptr[i] + (c == 0 ? 0 : len0);
+          const int32_t len = c == 0 ? len0 : len1;
+          for (int32_t a = 0; a < len; a++) lv.maps[ioff + (size_t)c * fm[i] + fwd[a]] = a;
+        }
+        const int32_t kp = (fk[i] + 3) & ~3;
         int32_t row[TF_PAT_WIDTH] = {fm[i], fk[i], nsrc, len0, len1, off0, off0 + len0,
-                                     L == 0 ? 1 : 0};
+                                     L == 0 ? 1 : 0, ioff, kp, fm[i] * kp + kp, 0};
         lv.pat.insert(lv.pat.end(), row, row + TF_PAT_WIDTH);
         bucket.push_back(found);
         lv.max_m = std::max(lv.max_m, fm[i]);

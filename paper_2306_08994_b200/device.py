@@ -34,6 +34,16 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def set_small_front_limit(m: int) -> int:
+    """Front order up to which levels use the shared-memory kernels (<= 232).
+
+    Lower values send levels through the blocked large-front kernels; tests
+    use this to drive the large path with the reference's small goldens.
+    Returns the previous limit.
+    """
+    return int(_lib.load().tf_set_small_max_m(int(m)))
+
+
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -45,7 +55,8 @@ class DeviceLevel:
         k = lt.pat[:, _lib.PAT_K].astype(np.int64)
         self.n_fronts = lt.n_fronts
         self.max_m = lt.max_m
-        self.fac_stride = int((m * k).max()) if len(m) else 0
+        fac = lt.pat[:, _lib.PAT_FAC].astype(np.int64)
+        self.fac_stride = int((fac.max() + 3) // 4 * 4) if len(fac) else 0  # 32-byte slots
         self.upd_stride = int(_tri(m - k).max()) if len(m) else 0
         self.pattern_of = torch.from_numpy(lt.pattern_of).to(device)
         self.piv_off = torch.from_numpy(lt.piv_off).to(device)
@@ -173,22 +184,13 @@ class DevicePlan:
                                        sp), "tf_permute_rows")
 
     def launches_per_factor(self) -> int:
-        """Kernel launches one factorization issues (small: 1/level; large: see factor_large.cu)."""
-        n = 0
+        """Kernel launches one factorization issues (tf_level_launch_count)."""
+        return sum(int(self.lib.tf_level_launch_count(C.byref(dl.view), 1, 0))
+                   for dl in self.levels)
+
+    def launches_per_solve(self, nrhs: int) -> int:
+        n = 2  # permutations
         for dl in self.levels:
-            if dl.max_m <= 232:
-                n += 1
-            else:
-                n += 3 + _panel_launches(dl.view.max_k) + (1 if dl.view.max_k > 0 else 0)
+            n += int(self.lib.tf_level_launch_count(C.byref(dl.view), nrhs, 1))
+            n += int(self.lib.tf_level_launch_count(C.byref(dl.view), nrhs, 2))
         return n
-
-
-def _panel_launches(k: int, nb: int = 64) -> int:
-    if k <= 0:
-        return 0
-    if k <= nb:
-        return 2
-    mid = (k // 2 + nb - 1) // nb * nb
-    if mid >= k:
-        mid = nb
-    return _panel_launches(mid, nb) + 1 + _panel_launches(k - mid, nb)

@@ -24,6 +24,7 @@ from typing import Optional
 import numpy as np
 import torch
 
+from . import _lib
 from .device import DevicePlan, require_cuda
 from .errors import ZeroPivotError
 
@@ -86,10 +87,10 @@ class FactorResult:
             fac = self.device_plan.factors[L].cpu().numpy()
             for i in range(lt.n_fronts):
                 row = lt.pat[lt.pattern_of[i]]
-                m, k = int(row[0]), int(row[1])
+                m, k, kp = int(row[_lib.PAT_M]), int(row[_lib.PAT_K]), int(row[_lib.PAT_KP])
                 if k == 0:
                     continue
-                P = fac[i * dl.fac_stride: i * dl.fac_stride + m * k].reshape(m, k)
+                P = fac[i * dl.fac_stride: i * dl.fac_stride + m * kp].reshape(m, kp)
                 lst = idx[ptr[i]:ptr[i + 1]]
                 pos = {int(g): r for r, g in enumerate(lst)}
                 for c in range(k):

@@ -30,9 +30,19 @@ def normwise(keys, vals, d):
     return np.abs(got - vals).max() / np.abs(vals).max()
 
 
+@pytest.fixture(params=["smem", "large"])
+def front_path(request, cuda_ok):
+    """Run with the default shared-memory kernels, or force every non-leaf level
+    through the blocked large-front (DMMA) kernels."""
+    from paper_2306_08994_b200.device import set_small_front_limit
+    old = set_small_front_limit(232 if request.param == "smem" else 1)
+    yield request.param
+    set_small_front_limit(old)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", SMALL)
-def test_factor_and_solve_match_reference(name, cuda_ok):
+def test_factor_and_solve_match_reference(name, front_path):
     g = golden(name)
     mesh, system, plan, state = pipeline(g)
     factors = tf.run_sequential(plan, state)
@@ -51,7 +61,7 @@ def test_factor_and_solve_match_reference(name, cuda_ok):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["2d_16x16_p2", "3d_4x4x4_p1", "1d_n1000_p1"])
-def test_multi_rhs_columnwise(name, cuda_ok):
+def test_multi_rhs_columnwise(name, front_path):
     g = golden(name)
     mesh, system, plan, state = pipeline(g)
     factors = tf.run_sequential(plan, state)
@@ -66,7 +76,7 @@ def test_multi_rhs_columnwise(name, cuda_ok):
 
 
 @pytest.mark.gpu
-def test_cfg2_against_reference_nested_loops(cuda_ok):
+def test_cfg2_against_reference_nested_loops(front_path):
     g = golden("2d_64x64_p2")
     mesh, system, plan, state = pipeline(g)
     factors = tf.run_sequential(plan, state)
