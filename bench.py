@@ -166,6 +166,9 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     tf, mesh, fronts, system, plan = build_problem(cfg)
+    if args.small_max_m is not None:
+        from paper_2306_08994_b200.device import set_small_front_limit
+        set_small_front_limit(args.small_max_m)
     state = tf.init_state(system, plan)
     dp = tf.compile_execution(plan, None, state)
     nrhs = cfg["nrhs"]
@@ -188,20 +191,10 @@ def run_ours(args, cfg):
     def step(ev=None):
         record = ev is not None
         dp.err.fill_(-1)
-        prev = None
         if record:
             ev[0].record(stream)
-        for L, dl in enumerate(dp.levels):
-            out = dp.upd[L & 1]
-            rc = lib.tf_level_factor(C.byref(dl.view),
-                                     None if prev is None else C.c_void_p(prev.data_ptr()),
-                                     C.c_void_p(dp.elem.data_ptr()),
-                                     C.c_void_p(dp.factors[L].data_ptr()),
-                                     C.c_void_p(out.data_ptr()), C.c_double(thr),
-                                     C.c_void_p(dp.err.data_ptr()), None, 0, sp)
-            if rc != 0:
-                raise RuntimeError(f"tf_level_factor failed at level {L}")
-            prev = out
+        for L in range(nl):
+            dp.factor_level(L, thr, sp)  # one Foata class: tf_level_factor
             if record:
                 ev[L + 1].record(stream)
         dp.solve_into(b, x, stream)
@@ -264,7 +257,7 @@ def run_ours(args, cfg):
     t_s = level_ms[L] / 1e3
     ridge = FP64_PEAK_TFLOPS * 1e12 / (hbm * 1e9)
     intensity = st["ldl_flops"] / max(st["bytes"], 1.0)
-    small = dp.levels[L].max_m <= 232  # default tf_set_small_max_m
+    small = not dp.levels[L].large
     kname = "factor_small_kernel" if small else "large level sequence (DMMA update/diag/trsm)"
     if intensity < ridge:
         roof = {"bound": "hbm", "achieved": st["bytes"] / t_s / 1e9, "peak": hbm, "unit": "GB/s"}
@@ -315,6 +308,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--small-max-m", type=int, default=None,
+                    help="tuning: largest front order kept on the shared-memory kernels")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

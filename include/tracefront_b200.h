@@ -126,9 +126,17 @@ typedef struct {
   const int64_t* piv_off;
   const int32_t* pat;
   const int32_t* maps;
+  double* aux;        /* large-front levels: per front, the unit-lower inverses of its
+                         64-wide diagonal blocks (ceil(k/64) x 64 x 64, row-major) */
+  int64_t aux_stride; /* doubles per front in aux (tf_level_aux_doubles) */
 } tf_level_view;
 
-/* Workspace bytes tf_level_factor needs for this level (0 for small fronts). */
+/* Doubles of `aux` each front of this level needs under the current
+ * shared-memory / large-front split (0 for shared-memory levels). */
+int64_t tf_level_aux_doubles(const tf_level_view* lv);
+
+/* Workspace bytes tf_level_factor / tf_level_solve_* need for this level with
+ * nrhs right-hand sides (0 when none). */
 int64_t tf_level_factor_workspace(const tf_level_view* lv);
 
 /* One Foata class (tree level) of the numeric factorization: extend-add of
@@ -162,7 +170,11 @@ int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,
  * vector, overwritten with x at this level's pivots. */
 int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
                        const double* factors, const double* x_parent, int64_t parent_rows,
-                       double* x_out, int64_t out_rows, double* y, int32_t nrhs, void* stream);
+                       double* x_out, int64_t out_rows, double* y, int32_t nrhs,
+                       void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Workspace bytes tf_level_solve_bwd needs for this level and nrhs. */
+int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs);
 
 /* out[i, :] = in[idx[i]-1, :] (natural -> pivot order); inverse when scatter != 0. */
 int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out, int32_t nrhs,

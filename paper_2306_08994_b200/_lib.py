@@ -51,6 +51,7 @@ class LevelView(C.Structure):
         ("child_upd_stride", C.c_int64), ("elem_stride", C.c_int64),
         ("pattern_of", C.c_void_p), ("piv_off", C.c_void_p),
         ("pat", C.c_void_p), ("maps", C.c_void_p),
+        ("aux", C.c_void_p), ("aux_stride", C.c_int64),
     ]
 
 
@@ -60,7 +61,7 @@ EXPORTS = (
     "tf_plan_level", "tf_plan_pivot_order", "tf_plan_node_lists", "tf_plan_node_lists_len",
     "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
     "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
-    "tf_build_info",
+    "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_build_info",
 )
 
 _lib = None
@@ -97,6 +98,8 @@ def load() -> C.CDLL:
     lib.tf_plan_node_lists_len.restype = i64
     lib.tf_level_factor_workspace.argtypes = [C.POINTER(LevelView)]
     lib.tf_level_factor_workspace.restype = i64
+    lib.tf_level_aux_doubles.argtypes = [C.POINTER(LevelView)]
+    lib.tf_level_aux_doubles.restype = i64
     lib.tf_level_factor.argtypes = [C.POINTER(LevelView), vp, vp, vp, vp, C.c_double, vp, vp,
                                     i64, vp]
     lib.tf_level_factor.restype = C.c_int
@@ -104,8 +107,10 @@ def load() -> C.CDLL:
                                        vp, i64, vp, i32, vp]
     lib.tf_level_solve_fwd.restype = C.c_int
     lib.tf_level_solve_bwd.argtypes = [C.POINTER(LevelView), C.POINTER(LevelView), vp, vp, i64,
-                                       vp, i64, vp, i32, vp]
+                                       vp, i64, vp, i32, vp, i64, vp]
     lib.tf_level_solve_bwd.restype = C.c_int
+    lib.tf_level_solve_workspace.argtypes = [C.POINTER(LevelView), i32]
+    lib.tf_level_solve_workspace.restype = i64
     lib.tf_permute_rows.argtypes = [vp, i64, vp, vp, i32, i32, vp]
     lib.tf_permute_rows.restype = C.c_int
     lib.tf_level_launch_count.argtypes = [C.POINTER(LevelView), i32, i32]

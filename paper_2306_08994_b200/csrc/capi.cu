@@ -4,7 +4,6 @@
 #include "common.cuh"
 
 namespace tfb {
-int small_smem_per_group(int max_m);
 cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, const double* elem,
                                 double* factors, double* upd_out, double thr,
                                 unsigned long long* err, cudaStream_t st);
@@ -17,12 +16,13 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
 cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_parent,
                              const double* factors, const double* x_parent, long long parent_rows,
                              double* x_out, long long out_rows, double* y, int nrhs,
-                             cudaStream_t st);
+                             double* work, long long work_doubles, cudaStream_t st);
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,
                                 int nrhs, int scatter, cudaStream_t st);
+long long solve_workspace_doubles(const LevelArgs& L, int nrhs);
 int large_panel_launches(int max_k);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
-int g_small_max_m = kSmallMaxM;
+int g_small_max_m = 112;  // measured best split on B200 (tools/sweep.sh)
 }  // namespace tfb
 
 using namespace tfb;
@@ -33,9 +33,19 @@ static int status(cudaError_t e) {
   return TF_ERR_CUDA;
 }
 
+extern "C" int64_t tf_level_aux_doubles(const tf_level_view* lv) {
+  if (!lv || !level_is_large(lv->is_leaf, lv->max_m) || lv->max_k <= 0) return 0;
+  return large_aux_doubles(lv->max_k);
+}
+
 extern "C" int64_t tf_level_factor_workspace(const tf_level_view* lv) {
   (void)lv;
   return 0;
+}
+
+extern "C" int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs) {
+  if (!lv || nrhs < 1) return 0;
+  return 8 * solve_workspace_doubles(make_args(lv), nrhs);
 }
 
 extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
@@ -50,8 +60,10 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
   if (!lv->is_leaf && !child_upd) return TF_ERR_INVALID;
   LevelArgs L = make_args(lv);
   cudaStream_t st = (cudaStream_t)stream;
-  if (lv->is_leaf || lv->max_m <= g_small_max_m)  // element fronts are always small
+  if (!level_is_large(lv->is_leaf, lv->max_m))
     return status(launch_factor_small(L, child_upd, elem, factors, upd_out, threshold, err, st));
+  if (lv->max_k > 0 && (!lv->aux || lv->aux_stride < large_aux_doubles(lv->max_k)))
+    return TF_ERR_INVALID;
   return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, st));
 }
 
@@ -71,14 +83,17 @@ extern "C" int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* 
 extern "C" int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
                                   const double* factors, const double* x_parent,
                                   int64_t parent_rows, double* x_out, int64_t out_rows,
-                                  double* y, int32_t nrhs, void* stream) {
+                                  double* y, int32_t nrhs, void* workspace,
+                                  int64_t workspace_bytes, void* stream) {
   if (!lv || nrhs < 1 || out_rows < lv->max_m || !x_out) return TF_ERR_INVALID;
   if (lv->n_fronts == 0) return TF_OK;
   if (parent && !x_parent) return TF_ERR_INVALID;
   LevelArgs L = make_args(lv);
   LevelArgs PA = parent ? make_args(parent) : L;
+  if (workspace_bytes < 8 * solve_workspace_doubles(L, nrhs)) return TF_ERR_INVALID;
   return status(launch_solve_bwd(L, PA, parent ? 1 : 0, factors, x_parent, parent_rows, x_out,
-                                 out_rows, y, nrhs, (cudaStream_t)stream));
+                                 out_rows, y, nrhs, (double*)workspace, workspace_bytes / 8,
+                                 (cudaStream_t)stream));
 }
 
 extern "C" int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out,
@@ -91,8 +106,8 @@ extern "C" int32_t tf_level_launch_count(const tf_level_view* lv, int32_t nrhs, 
   if (!lv || lv->n_fronts == 0) return 0;
   LevelArgs L = make_args(lv);
   if (phase == 0) {
-    if (lv->is_leaf || lv->max_m <= g_small_max_m) return 1;
-    return 3 + large_panel_launches(lv->max_k) + (lv->max_k > 0 && lv->max_upd > 0 ? 1 : 0);
+    if (!level_is_large(lv->is_leaf, lv->max_m)) return 1;
+    return 1 + large_panel_launches(lv->max_k) + (lv->max_k > 0 && lv->max_upd > 0 ? 1 : 0);
   }
   return solve_launches(L, nrhs, phase == 1);
 }
@@ -104,5 +119,6 @@ extern "C" int32_t tf_set_small_max_m(int32_t m) {
 }
 
 extern "C" const char* tf_build_info(void) {
-  return "tfb200 sm_100a fp64 (DMMA m8n8k4) small<=232 smem / large blocked";
+  return "tfb200 sm_100a fp64 (DMMA m8n8k4 via mma.sync; cp.async staging); "
+         "shared-memory fronts <= 232, blocked large fronts";
 }

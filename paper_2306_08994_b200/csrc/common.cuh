@@ -14,6 +14,9 @@ constexpr int kSmallMaxM = 232;
 // Runtime threshold (<= kSmallMaxM) between the shared-memory and the blocked
 // large-front paths; lowered by tests to drive the large path on small meshes.
 extern int g_small_max_m;
+// Per-front doubles of the diagonal-block inverses a large-front level keeps.
+long long large_aux_doubles(int max_k);
+inline bool level_is_large(int is_leaf, int max_m) { return !is_leaf && max_m > g_small_max_m; }
 
 // Kernel-side copy of tf_level_view (passed by value).
 struct LevelArgs {
@@ -31,6 +34,8 @@ struct LevelArgs {
   const long long* __restrict__ piv_off;
   const int* __restrict__ pat;
   const int* __restrict__ maps;
+  double* aux;
+  long long aux_stride;
 };
 
 inline LevelArgs make_args(const tf_level_view* v) {
@@ -49,6 +54,8 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.piv_off = reinterpret_cast<const long long*>(v->piv_off);
   a.pat = v->pat;
   a.maps = v->maps;
+  a.aux = v->aux;
+  a.aux_stride = v->aux_stride;
   return a;
 }
 

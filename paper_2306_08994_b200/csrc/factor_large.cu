@@ -1,14 +1,16 @@
 // Large-front level path (fronts too big for one SM's shared memory).
 //
 // Per level, batched over all fronts of the level (one launch per step):
-//   1. zero the factor slot (panel P, m x kp, + diagonal d) and the packed
-//      Schur block S in this level's update buffer;
-//   2. extend-add child 0 then child 1 (fixed order, no atomics);
-//   3. recursive blocked partial LDL^T of the k fully-summed columns:
-//      64-wide diagonal blocks factored in shared memory, row-parallel
-//      triangular solves below them, DMMA tile updates of the remaining
-//      panel columns;
-//   4. one DMMA update S -= L21 D L21^T over all k pivots.
+//   1. gather-form assembly: every entry of the panel P (m x kp), the diagonal
+//      vector d and the packed Schur block S is written exactly once, summing
+//      its child contributions through the inverse extend-add maps (fixed child
+//      order, no atomics, coalesced writes);
+//   2. recursive blocked partial LDL^T of the k fully-summed columns:
+//      a 64-wide diagonal block is factored in shared memory, which also
+//      forms its unit-lower inverse M (kept in `aux` for the solve); the rows
+//      below are solved as a DMMA GEMM  P_rb <- (P_rb M^T) D^-1; the remaining
+//      panel columns get DMMA rank-64.. updates;
+//   3. one DMMA update S -= L21 D L21^T over all k pivots.
 // Arithmetic replaced: engine.py:86-105 per pivot (Division, Multiplication,
 // Subtraction) and engine.py:537-545 (factorize_nested_loops inner loops).
 #include "common.cuh"
@@ -17,121 +19,143 @@ namespace tfb {
 
 constexpr int NB = 64;  // diagonal block width
 
-__global__ void large_zero_kernel(LevelArgs L, double* factors, double* upd) {
-  const long long f = blockIdx.y;
+__global__ void large_assemble_kernel(LevelArgs L, const double* __restrict__ child_upd,
+                                      double* __restrict__ factors, double* __restrict__ upd) {
+  const long long f = blockIdx.x;  // fronts on x (no 65535 limit), chunks on y
   const Shape s = front_shape(L, f);
-  const long long nP = (long long)s.m * s.kp + s.kp, nS = tri(s.m - s.k, 0);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long nPk = (long long)m * kp, nP = nPk + kp, nS = tri(m - k, 0);
   double* Pf = factors + f * L.fac_stride;
   double* Sf = upd + f * L.upd_stride;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nP + nS;
-       e += (long long)gridDim.x * blockDim.x) {
-    if (e < nP) Pf[e] = 0.0;
-    else Sf[e - nP] = 0.0;
+  const int* inv0 = L.maps + s.ioff;
+  const int* inv1 = inv0 + m;
+  const double* src0 = child_upd + (2 * f) * L.child_upd_stride;
+  const double* src1 = child_upd + (2 * f + 1) * L.child_upd_stride;
+  const bool two = s.nsrc == 2;
+  for (long long e = blockIdx.y * (long long)blockDim.x + threadIdx.x; e < nP + nS;
+       e += (long long)gridDim.y * blockDim.x) {
+    int r, c;
+    double* dst;
+    if (e < nPk) {
+      r = (int)(e / kp);
+      c = (int)(e - (long long)r * kp);
+      dst = Pf + e;
+      if (c >= k || c > r) { *dst = 0.0; continue; }
+    } else if (e < nP) {
+      Pf[e] = 0.0;
+      continue;
+    } else {
+      const long long e2 = e - nP;
+      const int a = tri_row(e2);
+      r = k + a;
+      c = k + (int)(e2 - tri(a, 0));
+      dst = Sf + e2;
+    }
+    double v = 0.0;
+    {
+      const int i = inv0[r], j = inv0[c];
+      if (i >= 0 && j >= 0) v += src0[i > j ? tri(i, j) : tri(j, i)];
+    }
+    if (two) {
+      const int i = inv1[r], j = inv1[c];
+      if (i >= 0 && j >= 0) v += src1[i > j ? tri(i, j) : tri(j, i)];
+    }
+    *dst = v;
   }
 }
 
-__global__ void large_scatter_kernel(LevelArgs L, const double* __restrict__ child_upd,
-                                     double* factors, double* upd, int c) {
-  const long long f = blockIdx.y;
-  const Shape s = front_shape(L, f);
-  if (c >= s.nsrc) return;
-  const int len = c == 0 ? s.len0 : s.len1;
-  const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
-  const double* src = child_upd + (2 * f + c) * L.child_upd_stride;
-  double* Pf = factors + f * L.fac_stride;
-  double* Sf = upd + f * L.upd_stride;
-  const long long n = tri(len, 0);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int a = tri_row(e), b = (int)(e - tri(a, 0));
-    const int R = mp[a], C = mp[b];
-    const int hi = R > C ? R : C, lo = R > C ? C : R;
-    const double v = src[e];
-    if (lo < s.k) Pf[(long long)hi * s.kp + lo] += v;
-    else Sf[tri(hi - s.k, lo - s.k)] += v;
-  }
-}
-
-// Factor the diagonal block [a, a+kb) of every front's panel in shared memory.
+// Factor the diagonal block [a, a+kb) of every front's panel (LDL^T, in shared
+// memory), store l (scaled) and d, and the unit-lower inverse M = L_bb^-1 in aux.
+// 256 threads: thread t owns row r = t/4, columns [16h, 16h+16) with h = t%4, held
+// in registers.  One barrier per pivot: the owners of column c publish it to a
+// double-buffered shared vector, every thread applies the rank-1 update to its
+// registers.  The inverse is formed the same way, one published row per step.
 __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* factors, int a,
                                                           double threshold,
                                                           unsigned long long* err) {
-  __shared__ double D[NB][NB + 1];
-  __shared__ double lv[NB];
+  constexpr int Q = 4, W = NB / Q;  // four threads per row, W columns each
+  __shared__ double buf[2][NB];
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(a + NB, s.k) - a;
   if (kb <= 0) return;
   double* Pf = factors + f * L.fac_stride;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < kb * NB; e += blockDim.x) {
-    const int i = e / NB, j = e - i * NB;
-    if (j <= i) D[i][j] = Pf[(long long)(a + i) * s.kp + a + j];
+  const int tid = threadIdx.x, r = tid / Q, h = tid % Q, c0 = h * W;
+  const int lane = tid & 31, quad = lane & ~(Q - 1);
+  double v[W];
+#pragma unroll
+  for (int j = 0; j < W; j++) {
+    const int col = c0 + j;
+    v[j] = (r < kb && col <= r) ? Pf[(long long)(a + r) * s.kp + a + col] : (r == col ? 1.0 : 0.0);
   }
-  __syncthreads();
   const long long piv0 = L.piv_off[f] + a;
-  for (int c = 0; c < kb; c++) {
-    const double d = D[c][c];
-    if (tid == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-    for (int r = c + 1 + tid; r < kb; r += blockDim.x) lv[r] = D[r][c] / d;
-    __syncthreads();
-    for (int r = c + 1 + warp; r < kb; r += 8) {
-      const double frc = D[r][c];
-      for (int q = c + 1 + lane; q <= r; q += 32) D[r][q] -= lv[q] * frc;
-      __syncwarp();
-      if (lane == 0) D[r][c] = lv[r];
+  // LDL^T: a(r,s) -= (a(s,c)/d) a(r,c); column c becomes l(r,c) = a(r,c)/d
+#pragma unroll
+  for (int c = 0; c < NB; c++) {
+    if (c < kb) {
+      double* cb = buf[c & 1];
+      if (h == c / W && r >= c) cb[r] = v[c % W];
+      __syncthreads();
+      const double d = cb[c];
+      if (tid == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
+      const double inv = 1.0 / d;
+      if (r > c && r < kb) {
+        const double arc = cb[r];
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const int col = c0 + j;
+          if (col > c && col <= r) v[j] -= (cb[col] * inv) * arc;
+        }
+        if (h == c / W) v[c % W] = arc * inv;
+      }
+    }
+  }
+  // write l (strict lower) and d back
+  if (r < kb) {
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+      const int col = c0 + j;
+      if (col <= r) Pf[(long long)(a + r) * s.kp + a + col] = v[j];
+    }
+    if (h == r / W) {
+#pragma unroll
+      for (int j = 0; j < W; j++)
+        if (c0 + j == r) Pf[(long long)s.m * s.kp + a + r] = v[j];
+    }
+  }
+  // unit-lower inverse M = L^-1, right-looking over rows t of M
+  double w[W];
+#pragma unroll
+  for (int j = 0; j < W; j++) w[j] = (c0 + j == r) ? 1.0 : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < NB - 1; t++) {
+    double* rb = buf[t & 1];
+    if (r == t) {
+#pragma unroll
+      for (int j = 0; j < W; j++) rb[c0 + j] = w[j];
     }
     __syncthreads();
+    // L[r][t] lives in the quad lane owning column block t / W
+    const double lrt = __shfl_sync(0xffffffffu, v[t % W], quad | (t / W));
+    if (r > t && r < kb) {
+#pragma unroll
+      for (int j = 0; j < W; j++)
+        if (c0 + j <= t) w[j] -= lrt * rb[c0 + j];
+    }
   }
-  for (int e = tid; e < kb * NB; e += blockDim.x) {
-    const int i = e / NB, j = e - i * NB;
-    if (j <= i) Pf[(long long)(a + i) * s.kp + a + j] = D[i][j];
-  }
-  double* dv = Pf + (long long)s.m * s.kp + a;
-  for (int c = tid; c < kb; c += blockDim.x) dv[c] = D[c][c];
+  double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
+#pragma unroll
+  for (int j = 0; j < W; j++) M[r * NB + c0 + j] = w[j];
 }
 
-// Row-parallel triangular solve below the diagonal block: row r, cols [a, a+kb):
-// for t: l_rt = a_rt / d_t; a_rc -= l_ct * a_rt (c > t).
-__global__ void __launch_bounds__(128) large_trsm_kernel(LevelArgs L, double* factors, int a) {
-  __shared__ double Lb[NB][NB + 1];
-  __shared__ double dinv[NB];
-  const long long f = blockIdx.y;
-  const Shape s = front_shape(L, f);
-  const int kb = min(a + NB, s.k) - a;
-  if (kb <= 0) return;
-  const int row0 = a + kb + blockIdx.x * blockDim.x;
-  if (row0 >= s.m) return;
-  double* Pf = factors + f * L.fac_stride;
-  for (int e = threadIdx.x; e < kb * NB; e += blockDim.x) {
-    const int i = e / NB, j = e - i * NB;
-    if (j < i) Lb[i][j] = Pf[(long long)(a + i) * s.kp + a + j];
-  }
-  for (int c = threadIdx.x; c < kb; c += blockDim.x) dinv[c] = 1.0 / Pf[(long long)(a + c) * s.kp + a + c];
-  __syncthreads();
-  const int r = row0 + threadIdx.x;
-  if (r >= s.m) return;
-  double x[NB];
-  double* row = Pf + (long long)r * s.kp + a;
-#pragma unroll
-  for (int t = 0; t < NB; t++) x[t] = t < kb ? row[t] : 0.0;
-#pragma unroll
-  for (int t = 0; t < NB; t++) {
-    const double v = x[t];
-    x[t] = v * dinv[t];
-#pragma unroll
-    for (int c = t + 1; c < NB; c++) x[c] -= Lb[c][t] * v;
-  }
-#pragma unroll
-  for (int t = 0; t < NB; t++)
-    if (t < kb) row[t] = x[t];
-}
-
-// C -= (A diag(d)) B^T with FP64 tensor-core MMA (mma.sync m8n8k4), 128x64
+// C (+)= op((A diag(d)) B^T) with FP64 tensor-core MMA (mma.sync m8n8k4): 128x64
 // CTA tiles, 8 warps of 32x32, 3-stage cp.async pipeline over K (BK = 16).
-// MODE 0 (panel): out P[r][c], r in [row0, m), c in [col0, min(col1, k)), r >= c,
-//                 A = P rows r, B = P rows c, K = [t0, min(t1, k)).
-// MODE 1 (schur): out S[i][j] packed, i >= j, A = P rows k+i, B = P rows k+j, K = [0, k).
+// MODE 0 (panel): P[r][c] -= sum_t l_rt d_t l_ct, r in [row0, m), c in [col0, min(col1,k)),
+//                 r >= c, t in [t0, min(t1, k)).
+// MODE 1 (schur): S[i][j] -= sum_t l_{k+i,t} d_t l_{k+j,t}, i >= j, t in [0, k).
+// MODE 2 (trsm) : P[r][t0+c] = (sum_t P[r][t0+t] M[c][t]) / d_{t0+c}, r >= t0+kb,
+//                 c < kb (M = unit-lower inverse of the diagonal block at t0).
 constexpr int GBM = 128, GBN = 64, GBK = 16, GLD = GBK + 4, GSTAGES = 3;
 
 template <int MODE>
@@ -142,68 +166,83 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
   double* As = gsm;                                  // [GSTAGES][GBM][GLD]
   double* Bs = As + GSTAGES * GBM * GLD;             // [GSTAGES][GBN][GLD]
   double* Ds = Bs + GSTAGES * GBN * GLD;             // [GSTAGES][GBK]
-  const long long f = blockIdx.z;
+  const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  int aRow0, bRow0, nA, nB, kBeg, kEnd;
+  double* Pf = factors + f * L.fac_stride;
+  const double* dvec = Pf + (long long)m * kp;
+  const double* Bbase = Pf;
+  int ldb = kp, aRow0, bRow0, nA, nB, aK0, bK0, kLen;
   long long tile_r0, tile_c0;
   if (MODE == 0) {
-    tile_r0 = row0 + (long long)blockIdx.y * GBM;
-    tile_c0 = col0 + (long long)blockIdx.x * GBN;
+    tile_r0 = row0 + (long long)blockIdx.z * GBM;
+    tile_c0 = col0 + (long long)blockIdx.y * GBN;
     const int cLim = min(col1, k);
     if (tile_r0 >= m || tile_c0 >= cLim || tile_r0 + GBM <= tile_c0) return;
     aRow0 = (int)tile_r0;
     bRow0 = (int)tile_c0;
     nA = min(GBM, m - aRow0);
     nB = min(GBN, cLim - bRow0);
-    kBeg = t0;
-    kEnd = min(t1, k);
-  } else {
+    aK0 = bK0 = t0;
+    kLen = min(t1, k) - t0;
+  } else if (MODE == 1) {
     const int u = m - k;
-    tile_r0 = (long long)blockIdx.y * GBM;
-    tile_c0 = (long long)blockIdx.x * GBN;
+    tile_r0 = (long long)blockIdx.z * GBM;
+    tile_c0 = (long long)blockIdx.y * GBN;
     if (tile_r0 >= u || tile_c0 >= u || tile_r0 + GBM <= tile_c0) return;
     aRow0 = k + (int)tile_r0;
     bRow0 = k + (int)tile_c0;
     nA = min(GBM, u - (int)tile_r0);
     nB = min(GBN, u - (int)tile_c0);
-    kBeg = 0;
-    kEnd = k;
+    aK0 = bK0 = 0;
+    kLen = k;
+  } else {
+    const int kb = min(t0 + NB, k) - t0;
+    if (kb <= 0) return;
+    tile_r0 = t0 + kb + (long long)blockIdx.z * GBM;
+    tile_c0 = t0;
+    if (tile_r0 >= m) return;
+    aRow0 = (int)tile_r0;
+    nA = min(GBM, m - aRow0);
+    Bbase = L.aux + f * L.aux_stride + (long long)(t0 / NB) * NB * NB;
+    ldb = NB;
+    bRow0 = 0;
+    nB = kb;
+    aK0 = t0;
+    bK0 = 0;
+    kLen = kb;
   }
-  if (kEnd <= kBeg) return;
-  const double* Pf = factors + f * L.fac_stride;
-  const double* dvec = Pf + (long long)m * kp;
+  if (kLen <= 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wy = warp >> 1, wx = warp & 1;  // 4 x 2 warps of 32x32
-  const int nk = (kEnd - kBeg + GBK - 1) / GBK;
+  const int nk = (kLen + GBK - 1) / GBK;
 
   auto issue = [&](int it) {
     const int stage = it % GSTAGES;
-    const int kt = kBeg + it * GBK;
+    const int kt = it * GBK;
     double* as = As + stage * GBM * GLD;
     double* bs = Bs + stage * GBN * GLD;
-    // A: 128 rows x 16 doubles = 1024 chunks of 2 doubles, 4 per thread
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < 4; q++) {  // A: 128 rows x 8 chunks of 2 doubles
       const int ch = tid + q * 256;
       const int r = ch >> 3, cc = (ch & 7) * 2;
       const int t = kt + cc;
-      const bool v = r < nA && t < kEnd;
-      const double* src = v ? Pf + (long long)(aRow0 + r) * kp + t : Pf;
+      const bool v = r < nA && t < kLen;
+      const double* src = v ? Pf + (long long)(aRow0 + r) * kp + aK0 + t : Pf;
       cp_async16(as + r * GLD + cc, src, v);
     }
 #pragma unroll
-    for (int q = 0; q < 2; q++) {
+    for (int q = 0; q < 2; q++) {  // B: 64 rows x 8 chunks
       const int ch = tid + q * 256;
       const int r = ch >> 3, cc = (ch & 7) * 2;
       const int t = kt + cc;
-      const bool v = r < nB && t < kEnd;
-      const double* src = v ? Pf + (long long)(bRow0 + r) * kp + t : Pf;
+      const bool v = r < nB && t < kLen;
+      const double* src = v ? Bbase + (long long)(bRow0 + r) * ldb + bK0 + t : Bbase;
       cp_async16(bs + r * GLD + cc, src, v);
     }
-    if (tid < GBK / 2) {
+    if (MODE != 2 && tid < GBK / 2) {
       const int t = kt + tid * 2;
-      cp_async16(Ds + stage * GBK + tid * 2, t < kEnd ? dvec + t : dvec, t < kEnd);
+      cp_async16(Ds + stage * GBK + tid * 2, t < kLen ? dvec + aK0 + t : dvec, t < kLen);
     }
   };
 
@@ -227,13 +266,17 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
     const double* as = As + stage * GBM * GLD + (wy * 32 + (lane >> 2)) * GLD + (lane & 3);
     const double* bs = Bs + stage * GBN * GLD + (wx * 32 + (lane >> 2)) * GLD + (lane & 3);
     const double* ds = Ds + stage * GBK + (lane & 3);
-    // K tail: entries past kEnd were zero-filled
 #pragma unroll
     for (int ks = 0; ks < GBK; ks += 4) {
-      const double dk = ds[ks];
       double af[4], bf[4];
+      if (MODE == 2) {
 #pragma unroll
-      for (int i = 0; i < 4; i++) af[i] = as[i * 8 * GLD + ks] * dk;
+        for (int i = 0; i < 4; i++) af[i] = as[i * 8 * GLD + ks];
+      } else {
+        const double dk = ds[ks];
+#pragma unroll
+        for (int i = 0; i < 4; i++) af[i] = as[i * 8 * GLD + ks] * dk;
+      }
 #pragma unroll
       for (int j = 0; j < 4; j++) bf[j] = bs[j * 8 * GLD + ks];
 #pragma unroll
@@ -243,8 +286,8 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
     }
   }
   cp_async_wait<0>();
-  // epilogue: C -= acc (lower part only)
-  double* out = MODE == 0 ? factors + f * L.fac_stride : upd + f * L.upd_stride;
+  if (MODE == 2) __syncthreads();  // every A tile row is read before it is overwritten
+  double* out = MODE == 1 ? upd + f * L.upd_stride : Pf;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const int rl = wy * 32 + i * 8 + (lane >> 2);
@@ -257,9 +300,13 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
         const int cl = wx * 32 + j * 8 + 2 * (lane & 3) + h;
         if (cl >= nB) continue;
         const long long C = tile_c0 + cl;
-        if (C > R) continue;
-        if (MODE == 0) out[R * kp + C] -= acc[i][j][h];
-        else out[tri(R, C)] -= acc[i][j][h];
+        if (MODE == 2) {
+          out[R * kp + C] = acc[i][j][h] / dvec[C];
+        } else {
+          if (C > R) continue;
+          if (MODE == 0) out[R * kp + C] -= acc[i][j][h];
+          else out[tri(R, C)] -= acc[i][j][h];
+        }
       }
     }
   }
@@ -272,16 +319,16 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
   if (b - a <= NB) {
     large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
     const int rows = L.max_m - a;
-    dim3 g((unsigned)((rows + 127) / 128), (unsigned)L.n_fronts);
-    large_trsm_kernel<<<g, 128, 0, st>>>(L, factors, a);
+    dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GBM - 1) / GBM));
+    large_update_kernel<2><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, 0, 0, 0, a, 0);
     return cudaGetLastError();
   }
   int mid = a + ((b - a) / 2 + NB - 1) / NB * NB;
   if (mid >= b) mid = a + NB;
   cudaError_t e = panel_factor(L, factors, thr, err, a, mid, st);
   if (e != cudaSuccess) return e;
-  dim3 g((unsigned)((b - mid + GBN - 1) / GBN), (unsigned)((L.max_m - mid + GBM - 1) / GBM),
-         (unsigned)L.n_fronts);
+  dim3 g((unsigned)L.n_fronts, (unsigned)((b - mid + GBN - 1) / GBN),
+         (unsigned)((L.max_m - mid + GBM - 1) / GBM));
   large_update_kernel<0><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, mid, mid, b, a, mid);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -292,24 +339,23 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                                 double* upd_out, double thr, unsigned long long* err,
                                 cudaStream_t st) {
   if (L.is_leaf) return cudaErrorInvalidValue;  // element fronts are never this large
+  if (L.max_k > 0 && (!L.aux || L.aux_stride < large_aux_doubles(L.max_k)))
+    return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(large_update_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
     cudaFuncSetAttribute(large_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
+    cudaFuncSetAttribute(large_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGemmSmem);
     attr = true;
   }
   {
     const long long per = L.fac_stride + tri(L.max_upd, 0);
     const unsigned gx = (unsigned)std::min<long long>((per + 255) / 256, 1024);
-    large_zero_kernel<<<dim3(gx, L.n_fronts), 256, 0, st>>>(L, factors, upd_out);
+    large_assemble_kernel<<<dim3(L.n_fronts, gx), 256, 0, st>>>(L, child_upd, factors, upd_out);
   }
-  const long long maxsrc = tri(L.max_m, 0);
-  const unsigned gx = (unsigned)std::min<long long>((maxsrc + 255) / 256, 2048);
-  for (int c = 0; c < 2; c++)
-    large_scatter_kernel<<<dim3(gx, L.n_fronts), 256, 0, st>>>(L, child_upd, factors, upd_out,
-                                                                c);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (L.max_k > 0) {
@@ -317,12 +363,16 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
     if (e != cudaSuccess) return e;
   }
   if (L.max_upd > 0 && L.max_k > 0) {
-    dim3 g((unsigned)((L.max_upd + GBN - 1) / GBN), (unsigned)((L.max_upd + GBM - 1) / GBM),
-           (unsigned)L.n_fronts);
+    dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + GBN - 1) / GBN),
+           (unsigned)((L.max_upd + GBM - 1) / GBM));
     large_update_kernel<1><<<g, 256, kGemmSmem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
     e = cudaGetLastError();
   }
   return e;
+}
+
+long long large_aux_doubles(int max_k) {
+  return (long long)((max_k + NB - 1) / NB) * NB * NB;
 }
 
 int large_panel_launches(int max_k) {

@@ -9,21 +9,30 @@
 // (zeros on shared rows) plus its children's update rows, eliminates its k
 // pivots and leaves rows [k, m) as its update for the parent.  The backward
 // sweep gathers the shared rows of x from the parent's block through the same
-// extend-add maps.  Small fronts: one thread group per front, block in shared
-// memory.  Large fronts: blocked (64-row diagonal solves + multi-CTA
-// matrix-vector updates), block in global memory.
+// extend-add maps.
+//   small fronts: one thread group per front, block in shared memory (RHS
+//                 columns processed in slices that fit);
+//   large fronts: blocked by the factorization's 64-wide diagonal blocks,
+//                 using their stored unit-lower inverses M (aux): forward
+//                 Y_b = M W_b then W_rows -= L_rows,b Y_b (one launch per
+//                 block); backward X_b = M^T (X_b - sum_rows L_rows,b^T X_rows)
+//                 with a deterministic two-pass reduction over row chunks.
 #include "common.cuh"
 
 namespace tfb {
 
-constexpr int SB = 64;  // diagonal block rows of the large-front sweeps
+constexpr int SB = 64;   // diagonal block rows (= factorization NB)
+constexpr int RB = 128;  // rows per CTA in the large-front row sweeps
 
 // ------------------------------------------------------------- small fronts
+// Vectors: row stride ldr (total RHS columns); this launch handles columns
+// [col0, col0 + nr).  Front blocks in w_in / w_out have the same row stride.
 template <int G, int GPC>
 __global__ void __launch_bounds__(G* GPC)
     solve_fwd_small(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
                     const double* __restrict__ w_child, long long child_rows, double* w_out,
-                    long long out_rows, double* y, int nrhs, int smem_per_group) {
+                    long long out_rows, double* y, int nr, int ldr, int col0,
+                    int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
@@ -33,8 +42,11 @@ __global__ void __launch_bounds__(G* GPC)
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
   const double* Lp = factors + f * L.fac_stride;
-  const int nW = m * nrhs, nK = k * nrhs;
-  for (int e = t; e < nW; e += G) W[e] = e < nK ? y[piv * nrhs + e] : 0.0;
+  const int nW = m * nr, nK = k * nr;
+  for (int e = t; e < nW; e += G) {
+    const int r = e / nr, j = e - r * nr;
+    W[e] = e < nK ? y[(piv + r) * ldr + col0 + j] : 0.0;
+  }
   group_sync<G>(bar);
   if (!L.is_leaf) {
     for (int c = 0; c < s.nsrc; c++) {
@@ -42,35 +54,42 @@ __global__ void __launch_bounds__(G* GPC)
       const int kc = C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
       const int len = c == 0 ? s.len0 : s.len1;
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
-      const double* Wc = w_child + ch * child_rows * nrhs + (long long)kc * nrhs;
-      const int n = len * nrhs;
+      const double* Wc = w_child + (ch * child_rows + kc) * ldr + col0;
+      const int n = len * nr;
       for (int e = t; e < n; e += G) {
-        const int a = e / nrhs, j = e - a * nrhs;
-        W[mp[a] * nrhs + j] += Wc[e];
+        const int a = e / nr, j = e - a * nr;
+        W[mp[a] * nr + j] += Wc[(long long)a * ldr + j];
       }
       group_sync<G>(bar);
     }
   }
   for (int c = 0; c < k; c++) {
-    const int n = (m - c - 1) * nrhs;
-    const double* Wc = W + c * nrhs;
+    const int n = (m - c - 1) * nr;
+    const double* Wc = W + c * nr;
     for (int e = t; e < n; e += G) {
-      const int r = c + 1 + e / nrhs, j = e % nrhs;
-      W[r * nrhs + j] -= Lp[(long long)r * kp + c] * Wc[j];
+      const int r = c + 1 + e / nr, j = e % nr;
+      W[r * nr + j] -= Lp[(long long)r * kp + c] * Wc[j];
     }
     group_sync<G>(bar);
   }
   const double* dv = Lp + (long long)m * kp;
-  for (int e = t; e < nK; e += G) y[piv * nrhs + e] = W[e] / dv[e / nrhs];
-  double* out = w_out + f * out_rows * nrhs;
-  for (int e = nK + t; e < nW; e += G) out[e] = W[e];
+  for (int e = t; e < nK; e += G) {
+    const int r = e / nr, j = e - r * nr;
+    y[(piv + r) * ldr + col0 + j] = W[e] / dv[r];
+  }
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int e = nK + t; e < nW; e += G) {
+    const int r = e / nr, j = e - r * nr;
+    out[(long long)r * ldr + j] = W[e];
+  }
 }
 
 template <int G, int GPC>
 __global__ void __launch_bounds__(G* GPC)
     solve_bwd_small(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
                     const double* __restrict__ x_parent, long long parent_rows, double* x_out,
-                    long long out_rows, double* y, int nrhs, int smem_per_group) {
+                    long long out_rows, double* y, int nr, int ldr, int col0,
+                    int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
@@ -80,42 +99,51 @@ __global__ void __launch_bounds__(G* GPC)
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
   const double* Lp = factors + f * L.fac_stride;
-  const int nW = m * nrhs, nK = k * nrhs;
-  for (int e = t; e < nK; e += G) X[e] = y[piv * nrhs + e];
+  const int nW = m * nr, nK = k * nr;
+  for (int e = t; e < nK; e += G) {
+    const int r = e / nr, j = e - r * nr;
+    X[e] = y[(piv + r) * ldr + col0 + j];
+  }
   if (has_parent && m > k) {
     const long long pf = f >> 1;
     const int c = (int)(f & 1);
     const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
     const int* mp = PA.maps + (c == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
-    const double* Xp = x_parent + pf * parent_rows * nrhs;
+    const double* Xp = x_parent + pf * parent_rows * ldr + col0;
     for (int e = nK + t; e < nW; e += G) {
-      const int a = (e - nK) / nrhs, j = (e - nK) % nrhs;
-      X[e] = Xp[(long long)mp[a] * nrhs + j];
+      const int a = (e - nK) / nr, j = (e - nK) % nr;
+      X[e] = Xp[(long long)mp[a] * ldr + j];
     }
   }
   group_sync<G>(bar);
   if (m > k) {
     for (int e = t; e < nK; e += G) {
-      const int c = e / nrhs, j = e - c * nrhs;
+      const int c = e / nr, j = e - c * nr;
       double acc = X[e];
-      for (int r = k; r < m; r++) acc -= Lp[(long long)r * kp + c] * X[r * nrhs + j];
+      for (int r = k; r < m; r++) acc -= Lp[(long long)r * kp + c] * X[r * nr + j];
       X[e] = acc;
     }
     group_sync<G>(bar);
   }
   for (int c = k - 1; c > 0; c--) {
-    const double* Xc = X + c * nrhs;
-    const int n = c * nrhs;
+    const double* Xc = X + c * nr;
+    const int n = c * nr;
     for (int e = t; e < n; e += G) {
-      const int r = e / nrhs, j = e - r * nrhs;
+      const int r = e / nr, j = e - r * nr;
       X[e] -= Lp[(long long)c * kp + r] * Xc[j];
     }
     group_sync<G>(bar);
   }
-  for (int e = t; e < nK; e += G) y[piv * nrhs + e] = X[e];
+  for (int e = t; e < nK; e += G) {
+    const int r = e / nr, j = e - r * nr;
+    y[(piv + r) * ldr + col0 + j] = X[e];
+  }
   if (!L.is_leaf) {
-    double* out = x_out + f * out_rows * nrhs;
-    for (int e = t; e < nW; e += G) out[e] = X[e];
+    double* out = x_out + f * out_rows * ldr + col0;
+    for (int e = t; e < nW; e += G) {
+      const int r = e / nr, j = e - r * nr;
+      out[(long long)r * ldr + j] = X[e];
+    }
   }
 }
 
@@ -123,84 +151,65 @@ __global__ void __launch_bounds__(G* GPC)
 __global__ void solve_gather_fwd(LevelArgs L, LevelArgs C, const double* __restrict__ w_child,
                                  long long child_rows, double* W, long long out_rows,
                                  const double* __restrict__ y, int nrhs) {
-  const long long f = blockIdx.y;
+  const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const long long piv = L.piv_off[f];
   const int nW = s.m * nrhs, nK = s.k * nrhs;
   int kc[2] = {0, 0};
-  for (int c = 0; c < s.nsrc && !L.is_leaf; c++)
+  for (int c = 0; c < s.nsrc; c++)
     kc[c] = C.pat[(size_t)C.pattern_of[2 * f + c] * TF_PAT_WIDTH + TF_PAT_K];
   double* Wf = W + f * out_rows * nrhs;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nW; e += gridDim.x * blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {
     const int r = e / nrhs, j = e - r * nrhs;
     double v = e < nK ? y[piv * nrhs + e] : 0.0;
-    if (!L.is_leaf) {
-      for (int c = 0; c < s.nsrc; c++) {
-        const int i = L.maps[s.ioff + c * s.m + r];
-        if (i >= 0)
-          v += w_child[(2 * f + c) * child_rows * nrhs + (long long)(kc[c] + i) * nrhs + j];
-      }
+    for (int c = 0; c < s.nsrc; c++) {
+      const int i = L.maps[s.ioff + c * s.m + r];
+      if (i >= 0) v += w_child[(2 * f + c) * child_rows * nrhs + (long long)(kc[c] + i) * nrhs + j];
     }
     Wf[e] = v;
   }
 }
 
-__global__ void __launch_bounds__(256) solve_fwd_diag(LevelArgs L, const double* __restrict__ factors,
-                                                       double* W, long long out_rows, double* y,
-                                                       int nrhs, int j0) {
+// Block j0: Y_b = M W_b (rows [j0, j0+kb)), y_b = Y_b / d; rows below: W_r -= L_r,b Y_b.
+__global__ void __launch_bounds__(256) solve_fwd_block(LevelArgs L, const double* __restrict__ factors,
+                                                        double* W, long long out_rows, double* y,
+                                                        int nrhs, int j0) {
   extern __shared__ __align__(16) double sm[];
-  double* Lb = sm;                 // [SB][SB+1]
-  double* Wb = sm + SB * (SB + 1); // [SB][nrhs]
+  double* Wb = sm;                 // [SB][nrhs] right-hand block
+  double* Yb = sm + SB * nrhs;     // [SB][nrhs] solved block
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(j0 + SB, s.k) - j0;
   if (kb <= 0) return;
+  const int j1 = j0 + kb;
+  const int r0 = j1 + blockIdx.y * RB;
+  if (blockIdx.y > 0 && r0 >= s.m) return;
   const double* Lp = factors + f * L.fac_stride;
+  const double* M = L.aux + f * L.aux_stride + (long long)(j0 / SB) * SB * SB;
   double* Wf = W + f * out_rows * nrhs;
-  for (int e = threadIdx.x; e < kb * SB; e += blockDim.x) {
-    const int i = e / SB, j = e - i * SB;
-    if (j < i) Lb[i * (SB + 1) + j] = Lp[(long long)(j0 + i) * s.kp + j0 + j];
-  }
   const int n = kb * nrhs;
   for (int e = threadIdx.x; e < n; e += blockDim.x) Wb[e] = Wf[(long long)j0 * nrhs + e];
   __syncthreads();
-  for (int c = 0; c < kb - 1; c++) {
-    const int nn = (kb - c - 1) * nrhs;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
-      const int r = c + 1 + e / nrhs, j = e % nrhs;
-      Wb[r * nrhs + j] -= Lb[r * (SB + 1) + c] * Wb[c * nrhs + j];
-    }
-    __syncthreads();
-  }
-  const double* dv = Lp + (long long)s.m * s.kp + j0;
-  const long long piv = L.piv_off[f] + j0;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    Wf[(long long)j0 * nrhs + e] = Wb[e];
-    y[piv * nrhs + e] = Wb[e] / dv[e / nrhs];
+    const int r = e / nrhs, j = e - r * nrhs;
+    const double* mr = M + r * SB;
+    double acc = Wb[e];  // M has a unit diagonal
+    for (int q = 0; q < r; q++) acc += mr[q] * Wb[q * nrhs + j];
+    Yb[e] = acc;
   }
-}
-
-__global__ void __launch_bounds__(256) solve_fwd_gemv(LevelArgs L, const double* __restrict__ factors,
-                                                       double* W, long long out_rows, int nrhs,
-                                                       int j0) {
-  extern __shared__ __align__(16) double sm[];  // Wb [SB][nrhs]
-  const long long f = blockIdx.y;
-  const Shape s = front_shape(L, f);
-  const int kb = min(j0 + SB, s.k) - j0;
-  if (kb <= 0) return;
-  const int r0 = j0 + kb + blockIdx.x * SB;
-  if (r0 >= s.m) return;
-  const double* Lp = factors + f * L.fac_stride;
-  double* Wf = W + f * out_rows * nrhs;
-  for (int e = threadIdx.x; e < kb * nrhs; e += blockDim.x) sm[e] = Wf[(long long)j0 * nrhs + e];
   __syncthreads();
-  const int rows = min(SB, s.m - r0);
+  if (blockIdx.y == 0) {
+    const double* dv = Lp + (long long)s.m * s.kp + j0;
+    const long long piv = L.piv_off[f] + j0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) y[piv * nrhs + e] = Yb[e] / dv[e / nrhs];
+  }
+  const int rows = min(RB, s.m - r0);
   for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) {
     const int rl = e / nrhs, j = e - rl * nrhs;
     const long long r = r0 + rl;
     const double* lrow = Lp + r * s.kp + j0;
     double acc = Wf[r * nrhs + j];
-    for (int q = 0; q < kb; q++) acc -= lrow[q] * sm[q * nrhs + j];
+    for (int q = 0; q < kb; q++) acc -= lrow[q] * Yb[q * nrhs + j];
     Wf[r * nrhs + j] = acc;
   }
 }
@@ -209,7 +218,7 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
                                  const double* __restrict__ x_parent, long long parent_rows,
                                  double* X, long long out_rows, const double* __restrict__ y,
                                  int nrhs) {
-  const long long f = blockIdx.y;
+  const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const long long piv = L.piv_off[f];
   const int nW = s.m * nrhs, nK = s.k * nrhs;
@@ -222,7 +231,7 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
     mp = PA.maps + ((f & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
     Xp = x_parent + pf * parent_rows * nrhs;
   }
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nW; e += gridDim.x * blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {
     if (e < nK) {
       Xf[e] = y[piv * nrhs + e];
     } else {
@@ -232,77 +241,67 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
   }
 }
 
-// X1[c][j] -= sum_{r in [k, m)} L[r][c] X[r][j]
-__global__ void solve_bwd_shared(LevelArgs L, const double* __restrict__ factors, double* X,
-                                 long long out_rows, int nrhs) {
-  const long long f = blockIdx.y;
-  const Shape s = front_shape(L, f);
-  if (s.m == s.k) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= s.k * nrhs) return;
-  const int j = e / s.k, c = e - j * s.k;  // c fastest: coalesced panel reads
-  const double* Lp = factors + f * L.fac_stride;
-  double* Xf = X + f * out_rows * nrhs;
-  double acc = Xf[(long long)c * nrhs + j];
-  for (int r = s.k; r < s.m; r++) acc -= Lp[(long long)r * s.kp + c] * Xf[(long long)r * nrhs + j];
-  Xf[(long long)c * nrhs + j] = acc;
-}
-
-__global__ void __launch_bounds__(256) solve_bwd_diag(LevelArgs L, const double* __restrict__ factors,
-                                                       double* X, long long out_rows, double* y,
-                                                       int nrhs, int j0) {
-  extern __shared__ __align__(16) double sm[];
-  double* Lb = sm;
-  double* Xb = sm + SB * (SB + 1);
+// partial[f][x][c][j] = sum_{r in chunk x of [j1, m)} L[r][j0+c] X[r][j]
+__global__ void __launch_bounds__(256) solve_bwd_partial(LevelArgs L, const double* __restrict__ factors,
+                                                          const double* __restrict__ X,
+                                                          long long out_rows, int nrhs, int j0,
+                                                          double* partial, int nchunk) {
+  extern __shared__ __align__(16) double sm[];  // Xr [RB][nrhs]
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(j0 + SB, s.k) - j0;
   if (kb <= 0) return;
-  const double* Lp = factors + f * L.fac_stride;
-  double* Xf = X + f * out_rows * nrhs;
-  for (int e = threadIdx.x; e < kb * SB; e += blockDim.x) {
-    const int i = e / SB, j = e - i * SB;
-    if (j < i) Lb[i * (SB + 1) + j] = Lp[(long long)(j0 + i) * s.kp + j0 + j];
-  }
+  const int j1 = j0 + kb;
+  const int r0 = j1 + blockIdx.y * RB;
+  double* P = partial + ((f * nchunk + blockIdx.y) * SB) * (long long)nrhs;
   const int n = kb * nrhs;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) Xb[e] = Xf[(long long)j0 * nrhs + e];
-  __syncthreads();
-  for (int c = kb - 1; c > 0; c--) {
-    const int nn = c * nrhs;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
-      const int r = e / nrhs, j = e - r * nrhs;
-      Xb[e] -= Lb[c * (SB + 1) + r] * Xb[c * nrhs + j];
-    }
-    __syncthreads();
+  if (r0 >= s.m) {
+    for (int e = threadIdx.x; e < n; e += blockDim.x) P[e] = 0.0;
+    return;
   }
-  const long long piv = L.piv_off[f] + j0;
+  const double* Lp = factors + f * L.fac_stride;
+  const double* Xf = X + f * out_rows * nrhs;
+  const int rows = min(RB, s.m - r0);
+  for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) sm[e] = Xf[(long long)r0 * nrhs + e];
+  __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    Xf[(long long)j0 * nrhs + e] = Xb[e];
-    y[piv * nrhs + e] = Xb[e];
+    const int j = e / kb, c = e - j * kb;  // c fastest: coalesced panel reads
+    const double* lcol = Lp + (long long)r0 * s.kp + j0 + c;
+    double acc = 0.0;
+    for (int q = 0; q < rows; q++) acc += lcol[(long long)q * s.kp] * sm[q * nrhs + j];
+    P[c * nrhs + j] = acc;
   }
 }
 
-// X[c][j] -= sum_{t < kb} L[j0+t][c] X[j0+t][j] for c < j0
-__global__ void __launch_bounds__(256) solve_bwd_gemv(LevelArgs L, const double* __restrict__ factors,
-                                                       double* X, long long out_rows, int nrhs,
-                                                       int j0) {
-  extern __shared__ __align__(16) double sm[];  // Xb [SB][nrhs]
-  const long long f = blockIdx.y;
+// X_b = M^T (X_b - sum_x partial[x]); writes X rows [j0, j0+kb) and y.
+__global__ void __launch_bounds__(256) solve_bwd_block(LevelArgs L, double* X, long long out_rows,
+                                                        double* y, int nrhs, int j0,
+                                                        const double* __restrict__ partial,
+                                                        int nchunk) {
+  extern __shared__ __align__(16) double sm[];  // Rb [SB][nrhs]
+  const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(j0 + SB, s.k) - j0;
   if (kb <= 0) return;
-  const double* Lp = factors + f * L.fac_stride;
+  const int j1 = j0 + kb;
+  const int used = s.m > j1 ? (s.m - j1 + RB - 1) / RB : 0;
+  const double* M = L.aux + f * L.aux_stride + (long long)(j0 / SB) * SB * SB;
   double* Xf = X + f * out_rows * nrhs;
-  const int e0 = blockIdx.x * blockDim.x;
-  if (e0 >= j0 * nrhs) return;
-  for (int e = threadIdx.x; e < kb * nrhs; e += blockDim.x) sm[e] = Xf[(long long)j0 * nrhs + e];
+  const int n = kb * nrhs;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    double v = Xf[(long long)j0 * nrhs + e];
+    for (int x = 0; x < used; x++) v -= partial[((f * nchunk + x) * SB) * (long long)nrhs + e];
+    sm[e] = v;
+  }
   __syncthreads();
-  const int e = e0 + threadIdx.x;
-  if (e >= j0 * nrhs) return;
-  const int j = e / j0, c = e - j * j0;
-  double acc = Xf[(long long)c * nrhs + j];
-  for (int q = 0; q < kb; q++) acc -= Lp[(long long)(j0 + q) * s.kp + c] * sm[q * nrhs + j];
-  Xf[(long long)c * nrhs + j] = acc;
+  const long long piv = L.piv_off[f] + j0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int c = e / nrhs, j = e - c * nrhs;
+    double acc = sm[e];  // (M^T)[c][c] = 1
+    for (int q = c + 1; q < kb; q++) acc += M[q * SB + c] * sm[q * nrhs + j];
+    Xf[(long long)j0 * nrhs + e] = acc;
+    y[piv * nrhs + e] = acc;
+  }
 }
 
 __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
@@ -320,32 +319,35 @@ __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
 }
 
 // ------------------------------------------------------------------ launch
-static bool small_solve_ok(const LevelArgs& L, int nrhs) {
-  return L.max_m <= g_small_max_m && (size_t)L.max_m * nrhs * 8 <= 200 * 1024;
-}
+constexpr size_t kSmallSolveSmem = 160 * 1024;
 
 template <int G, int GPC, bool FWD>
 static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, int flag,
                                       const double* factors, const double* w_in,
                                       long long in_rows, double* w_out, long long out_rows,
-                                      double* y, int nrhs, cudaStream_t st) {
-  const int per = (int)(((size_t)L.max_m * nrhs * 8 + 15) & ~(size_t)15);
+                                      double* y, int nr, int ldr, int col0, cudaStream_t st) {
+  const int per = (int)(((size_t)L.max_m * nr * 8 + 15) & ~(size_t)15);
   const size_t smem = (size_t)per * GPC;
   const unsigned blocks = (unsigned)((L.n_fronts + GPC - 1) / GPC);
   if (FWD) {
     auto kern = solve_fwd_small<G, GPC>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<blocks, G * GPC, smem, st>>>(L, O, factors, w_in, in_rows, w_out, out_rows, y, nrhs,
-                                        per);
+    kern<<<blocks, G * GPC, smem, st>>>(L, O, factors, w_in, in_rows, w_out, out_rows, y, nr, ldr,
+                                        col0, per);
   } else {
     auto kern = solve_bwd_small<G, GPC>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<blocks, G * GPC, smem, st>>>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y,
-                                        nrhs, per);
+                                        nr, ldr, col0, per);
   }
   return cudaGetLastError();
+}
+
+static int small_cols(const LevelArgs& L, int nrhs) {
+  const int cmax = (int)(kSmallSolveSmem / (8 * (size_t)std::max(L.max_m, 1)));
+  return std::max(1, std::min(nrhs, cmax));
 }
 
 template <bool FWD>
@@ -353,37 +355,48 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
                                   const double* factors, const double* w_in, long long in_rows,
                                   double* w_out, long long out_rows, double* y, int nrhs,
                                   cudaStream_t st) {
-  const long long work = (long long)L.max_m * nrhs;
-  const long long bytes = work * 8;
-#define TFB_SMALL(G, GPC) \
-  launch_small_solve<G, GPC, FWD>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nrhs, st)
-  if (work <= 16 && bytes * 32 <= 160 * 1024) return TFB_SMALL(8, 32);
-  if (work <= 64 && bytes * 16 <= 160 * 1024) return TFB_SMALL(16, 16);
-  if (work <= 256 && bytes * 8 <= 160 * 1024) return TFB_SMALL(32, 8);
-  if (work <= 2048 && bytes * 2 <= 160 * 1024) return TFB_SMALL(128, 2);
-  return TFB_SMALL(256, 1);
+  const int cw = small_cols(L, nrhs);
+  for (int col0 = 0; col0 < nrhs; col0 += cw) {
+    const int nr = std::min(cw, nrhs - col0);
+    const long long work = (long long)L.max_m * nr;
+    const long long bytes = work * 8;
+    cudaError_t e;
+#define TFB_SMALL(G, GPC)                                                                  \
+  launch_small_solve<G, GPC, FWD>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nr, \
+                                  nrhs, col0, st)
+    if (work <= 16 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
+    else if (work <= 64 && bytes * 16 <= (long long)kSmallSolveSmem) e = TFB_SMALL(16, 16);
+    else if (work <= 256 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
+    else if (work <= 2048 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
+    else e = TFB_SMALL(256, 1);
 #undef TFB_SMALL
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+long long solve_workspace_doubles(const LevelArgs& L, int nrhs) {
+  if (!level_is_large(L.is_leaf, L.max_m)) return 0;
+  const long long nchunk = (L.max_m + RB - 1) / RB;
+  return (long long)L.n_fronts * nchunk * SB * nrhs;
 }
 
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
                              long long out_rows, double* y, int nrhs, cudaStream_t st) {
-  if (small_solve_ok(L, nrhs))
+  if (!level_is_large(L.is_leaf, L.max_m))
     return dispatch_small<true>(L, C, 0, factors, w_child, child_rows, w_out, out_rows, y, nrhs,
                                 st);
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
-  solve_gather_fwd<<<dim3((unsigned)std::min<long long>((nW + 255) / 256, 1024), nf), 256, 0,
+  solve_gather_fwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, C, w_child, child_rows, w_out, out_rows, y, nrhs);
-  const size_t sm_diag = sizeof(double) * (SB * (SB + 1) + (size_t)SB * nrhs);
-  const size_t sm_gemv = sizeof(double) * (size_t)SB * nrhs;
-  cudaFuncSetAttribute(solve_fwd_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_diag);
-  cudaFuncSetAttribute(solve_fwd_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_gemv);
+  const size_t smem = sizeof(double) * 2 * SB * (size_t)nrhs;
+  cudaFuncSetAttribute(solve_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int j0 = 0; j0 < L.max_k; j0 += SB) {
-    solve_fwd_diag<<<nf, 256, sm_diag, st>>>(L, factors, w_out, out_rows, y, nrhs, j0);
-    const int rows = L.max_m - j0;
-    solve_fwd_gemv<<<dim3((unsigned)((rows + SB - 1) / SB), nf), 256, sm_gemv, st>>>(
-        L, factors, w_out, out_rows, nrhs, j0);
+    const int rows = std::max(1, L.max_m - j0 - 1);
+    solve_fwd_block<<<dim3(nf, (unsigned)((rows + RB - 1) / RB)), 256, smem, st>>>(
+        L, factors, w_out, out_rows, y, nrhs, j0);
   }
   return cudaGetLastError();
 }
@@ -391,38 +404,36 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
 cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_parent,
                              const double* factors, const double* x_parent, long long parent_rows,
                              double* x_out, long long out_rows, double* y, int nrhs,
-                             cudaStream_t st) {
-  if (small_solve_ok(L, nrhs))
+                             double* work, long long work_doubles, cudaStream_t st) {
+  if (!level_is_large(L.is_leaf, L.max_m))
     return dispatch_small<false>(L, PA, has_parent, factors, x_parent, parent_rows, x_out,
                                  out_rows, y, nrhs, st);
+  if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
-  solve_gather_bwd<<<dim3((unsigned)std::min<long long>((nW + 255) / 256, 1024), nf), 256, 0,
+  solve_gather_bwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, PA, has_parent, x_parent, parent_rows, x_out, out_rows, y, nrhs);
-  const long long nK = (long long)L.max_k * nrhs;
-  solve_bwd_shared<<<dim3((unsigned)((nK + 127) / 128), nf), 128, 0, st>>>(L, factors, x_out,
-                                                                            out_rows, nrhs);
-  const size_t sm_diag = sizeof(double) * (SB * (SB + 1) + (size_t)SB * nrhs);
-  const size_t sm_gemv = sizeof(double) * (size_t)SB * nrhs;
-  cudaFuncSetAttribute(solve_bwd_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_diag);
-  cudaFuncSetAttribute(solve_bwd_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_gemv);
+  const int nchunk = (L.max_m + RB - 1) / RB;
+  const size_t smp = sizeof(double) * RB * (size_t)nrhs;
+  const size_t smb = sizeof(double) * SB * (size_t)nrhs;
+  cudaFuncSetAttribute(solve_bwd_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+  cudaFuncSetAttribute(solve_bwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
   const int nblk = (L.max_k + SB - 1) / SB;
   for (int b = nblk - 1; b >= 0; b--) {
     const int j0 = b * SB;
-    solve_bwd_diag<<<nf, 256, sm_diag, st>>>(L, factors, x_out, out_rows, y, nrhs, j0);
-    if (j0 > 0) {
-      const long long n = (long long)j0 * nrhs;
-      solve_bwd_gemv<<<dim3((unsigned)((n + 255) / 256), nf), 256, sm_gemv, st>>>(
-          L, factors, x_out, out_rows, nrhs, j0);
-    }
+    const int rows = std::max(1, L.max_m - j0 - 1);
+    const int used = (rows + RB - 1) / RB;
+    solve_bwd_partial<<<dim3(nf, (unsigned)used), 256, smp, st>>>(L, factors, x_out, out_rows,
+                                                                  nrhs, j0, work, nchunk);
+    solve_bwd_block<<<nf, 256, smb, st>>>(L, x_out, out_rows, y, nrhs, j0, work, nchunk);
   }
   return cudaGetLastError();
 }
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
-  if (small_solve_ok(L, nrhs)) return 1;
+  if (!level_is_large(L.is_leaf, L.max_m)) return (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
   const int nblk = (L.max_k + SB - 1) / SB;
-  return fwd ? 1 + 2 * nblk : 2 + nblk + (nblk > 0 ? nblk - 1 : 0);
+  return fwd ? 1 + nblk : 1 + 2 * nblk;
 }
 
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,

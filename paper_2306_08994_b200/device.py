@@ -7,8 +7,11 @@ one Foata class (tree level) per `tf_level_factor` call, in stream order
 (the stream is the class barrier of engine.py:330-332).
 
 Device memory layout per level L (all float64, row-major):
-  factors[L] : n_fronts x fac_stride    front panel P (m x k), lower part valid
-  upd ping-pong: n_fronts x upd_stride  packed lower Schur complement (m-k)^2
+  factors[L] : n_fronts x fac_stride   front panel P (m x kp, lower part valid)
+                                       followed by the pivots d (kp)
+  aux[L]     : n_fronts x aux_stride   large-front levels only: unit-lower
+                                       inverses of the 64-wide diagonal blocks
+  upd ping-pong: n_fronts x upd_stride packed lower Schur complement (m-k)^2
   solve blocks : n_fronts x max_m x nrhs (forward W / backward X, ping-pong)
 """
 
@@ -39,7 +42,7 @@ def set_small_front_limit(m: int) -> int:
 
     Lower values send levels through the blocked large-front kernels; tests
     use this to drive the large path with the reference's small goldens.
-    Returns the previous limit.
+    Set it before `compile_execution`.  Returns the previous limit.
     """
     return int(_lib.load().tf_set_small_max_m(int(m)))
 
@@ -49,7 +52,7 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 class DeviceLevel:
-    def __init__(self, lt, device, child_upd_stride: int, elem_stride: int, elem_ld: int):
+    def __init__(self, lib, lt, device, child_upd_stride: int, elem_stride: int, elem_ld: int):
         self.tables = lt
         m = lt.pat[:, _lib.PAT_M].astype(np.int64)
         k = lt.pat[:, _lib.PAT_K].astype(np.int64)
@@ -80,7 +83,18 @@ class DeviceLevel:
         v.piv_off = self.piv_off.data_ptr()
         v.pat = self.pat.data_ptr()
         v.maps = self.maps.data_ptr()
+        self.aux_stride = int(lib.tf_level_aux_doubles(C.byref(v)))
+        self.aux = None
+        if self.aux_stride > 0:
+            self.aux = torch.empty(self.n_fronts * self.aux_stride, dtype=torch.float64,
+                                   device=device)
+            v.aux = self.aux.data_ptr()
+            v.aux_stride = self.aux_stride
         self.view = v
+
+    @property
+    def large(self) -> bool:
+        return self.aux_stride > 0
 
 
 class DevicePlan:
@@ -98,7 +112,7 @@ class DevicePlan:
         self.levels: list[DeviceLevel] = []
         child = 0
         for lt in native.levels:
-            dl = DeviceLevel(lt, self.device, child, elem_stride, elem_ld)
+            dl = DeviceLevel(self.lib, lt, self.device, child, elem_stride, elem_ld)
             self.levels.append(dl)
             child = dl.upd_stride
         self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)
@@ -112,20 +126,21 @@ class DevicePlan:
         self._blk = None
 
     # ---- factorization -----------------------------------------------------------
+    def factor_level(self, L: int, threshold: float, sp) -> None:
+        dl = self.levels[L]
+        prev = self.upd[(L - 1) & 1] if L > 0 else None
+        rc = self.lib.tf_level_factor(C.byref(dl.view), _ptr(prev), _ptr(self.elem),
+                                      _ptr(self.factors[L]), _ptr(self.upd[L & 1]),
+                                      C.c_double(threshold), _ptr(self.err), None, 0, sp)
+        _lib.check(rc, f"tf_level_factor(level {L})")
+
     def factor(self, threshold: float, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Enqueue every level on `stream`; no host synchronisation."""
         st = stream or torch.cuda.current_stream(self.device)
         sp = C.c_void_p(st.cuda_stream)
         self.err.fill_(-1)
-        lib = self.lib
-        prev = None
-        for L, dl in enumerate(self.levels):
-            out = self.upd[L & 1]
-            rc = lib.tf_level_factor(C.byref(dl.view), _ptr(prev), _ptr(self.elem),
-                                     _ptr(self.factors[L]), _ptr(out), C.c_double(threshold),
-                                     _ptr(self.err), None, 0, sp)
-            _lib.check(rc, f"tf_level_factor(level {L})")
-            prev = out
+        for L in range(len(self.levels)):
+            self.factor_level(L, threshold, sp)
 
     def zero_pivot_position(self) -> int:
         """-1, or the pivot-order position of the earliest pivot at/below threshold."""
@@ -139,6 +154,10 @@ class DevicePlan:
                          for _ in range(2)]
             self._y = torch.empty(max(1, self.n_pivots * nrhs), dtype=torch.float64,
                                   device=self.device)
+            ws = max(int(self.lib.tf_level_solve_workspace(C.byref(dl.view), nrhs))
+                     for dl in self.levels)
+            self._ws = torch.empty(max(1, ws // 8), dtype=torch.float64, device=self.device)
+            self._ws_bytes = ws
             self._solve_nrhs = nrhs
         return self._blk
 
@@ -177,7 +196,7 @@ class DevicePlan:
                                         C.byref(parent.view) if parent else None,
                                         _ptr(self.factors[L]), _ptr(prev),
                                         parent.max_m if parent else 0, _ptr(cur), dl.max_m,
-                                        _ptr(y), nrhs, sp)
+                                        _ptr(y), nrhs, _ptr(self._ws), self._ws_bytes, sp)
             _lib.check(rc, f"tf_level_solve_bwd(level {L})")
             prev = cur
         _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(y), _ptr(x), nrhs, 1,
