@@ -11,12 +11,25 @@
 // tasks.py:114-130).  The front is symmetric, so only its lower triangle is
 // kept (packed, row-major) and l(x,z) = q(z,x) is stored once.
 //
+// Phases: (1) extend-add of the sources, each thread streaming one contiguous
+// chunk of a source's packed triangle; (2) right-looking factorization of the
+// k pivot columns only (panel); (3) the Schur block S -= L21 D L21^T in one
+// pass -- FP64 tensor-core MMA (mma.sync m8n8k4, 8x8 tiles per warp) when
+// the group is at least a warp, FMA otherwise; (4) contiguous copy-out.
+//
 // Output per front: factor slot = panel P (m x kp row-major; P[r][c] = l(r,c)
 // for r > c, P[c][c] = d_c) followed by d (kp doubles); update slot = packed
 // lower (m-k)^2 Schur complement.
 #include "common.cuh"
 
 namespace tfb {
+
+// Thread t's contiguous chunk [beg, end) of n items split over G threads.
+__device__ __forceinline__ void chunk_of(int n, int G, int t, int& beg, int& end) {
+  const int c = (n + G - 1) / G;
+  beg = min(n, t * c);
+  end = min(n, beg + c);
+}
 
 template <int G, int GPC>
 __global__ void __launch_bounds__(G* GPC)
@@ -37,7 +50,7 @@ __global__ void __launch_bounds__(G* GPC)
   int* mp = reinterpret_cast<int*>(lv + mm);
 
   const Shape S = front_shape(L, f);
-  const int m = S.m, k = S.k, kp = S.kp;
+  const int m = S.m, k = S.k, kp = S.kp, u = m - k;
   const int nF = (int)tri(m, 0);
 
   for (int e = t; e < nF; e += G) F[e] = 0.0;
@@ -45,76 +58,137 @@ __global__ void __launch_bounds__(G* GPC)
   for (int i = t; i < S.len1; i += G) mp[S.len0 + i] = L.maps[S.off1 + i];
   group_sync<G>(bar);
 
-  // extend-add: each source entry read once (coalesced), scattered into F;
-  // sources in fixed order, no atomics.
+  // (1) extend-add: sources in fixed order, no atomics
   for (int c = 0; c < S.nsrc; c++) {
     const int len = c == 0 ? S.len0 : S.len1;
     const int* cm = mp + (c == 0 ? 0 : S.len0);
     const int n = (int)tri(len, 0);
-    if (L.is_leaf) {
-      const double* E = elem + f * L.elem_stride;
-      for (int e = t; e < n; e += G) {
-        const int a = tri_row(e), b = e - (int)tri(a, 0);
-        const int R = cm[a], C = cm[b];
-        F[R > C ? tri(R, C) : tri(C, R)] += E[a * L.elem_ld + b];
-      }
-    } else {
-      const double* src = child_upd + (2 * f + c) * L.child_upd_stride;
-      for (int e = t; e < n; e += G) {
-        const int a = tri_row(e), b = e - (int)tri(a, 0);
-        const int R = cm[a], C = cm[b];
-        F[R > C ? tri(R, C) : tri(C, R)] += src[e];
+    int beg, end;
+    chunk_of(n, G, t, beg, end);
+    if (beg < end) {
+      int a = tri_row(beg), b = beg - (int)tri(a, 0);
+      if (L.is_leaf) {
+        const double* E = elem + f * L.elem_stride;
+        for (int e = beg; e < end; e++) {
+          const int R = cm[a], C = cm[b];
+          F[R > C ? tri(R, C) : tri(C, R)] += E[a * L.elem_ld + b];
+          if (++b > a) { a++; b = 0; }
+        }
+      } else {
+        const double* src = child_upd + (2 * f + c) * L.child_upd_stride;
+        constexpr int U = 4;
+        int e = beg;
+        for (; e + U <= end; e += U) {
+          double v[U];
+#pragma unroll
+          for (int q = 0; q < U; q++) v[q] = __ldg(src + e + q);
+#pragma unroll
+          for (int q = 0; q < U; q++) {
+            const int R = cm[a], C = cm[b];
+            F[R > C ? tri(R, C) : tri(C, R)] += v[q];
+            if (++b > a) { a++; b = 0; }
+          }
+        }
+        for (; e < end; e++) {
+          const int R = cm[a], C = cm[b];
+          F[R > C ? tri(R, C) : tri(C, R)] += __ldg(src + e);
+          if (++b > a) { a++; b = 0; }
+        }
       }
     }
     group_sync<G>(bar);
   }
 
-  // partial LDL^T of the k eliminable pivots (right-looking, rank 1 per pivot)
+  // (2) panel: right-looking over the k pivot columns, updates confined to them
   const long long piv0 = L.piv_off[f];
   for (int c = 0; c < k; c++) {
     const double d = F[tri(c, c)];
     if (t == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
     for (int r = c + 1 + t; r < m; r += G) lv[r] = F[tri(r, c)] / d;
     group_sync<G>(bar);
+    for (int r = c + 1 + t; r < m; r += G) {
+      double* row = F + tri(r, 0);
+      const double frc = row[c];
+      const int smax = min(r, k - 1);
+      for (int s = c + 1; s <= smax; s++) row[s] -= lv[s] * frc;
+      row[c] = lv[r];
+    }
+    group_sync<G>(bar);
+  }
+
+  // (3) Schur block: F[k+i][k+j] -= sum_t l(k+i,t) d_t l(k+j,t), i >= j
+  if (k > 0 && u > 0) {
+    for (int c = t; c < k; c += G) lv[c] = F[tri(c, c)];  // pivots
+    group_sync<G>(bar);
     if constexpr (G >= 32) {
-      const int warp = t >> 5, lane = t & 31;
-      for (int r = c + 1 + warp; r < m; r += G / 32) {
-        double* row = F + tri(r, 0);
-        const double frc = row[c];
-        for (int s = c + 1 + lane; s <= r; s += 32) row[s] -= lv[s] * frc;
-        __syncwarp();
-        if (lane == 0) row[c] = lv[r];
+      const int warp = t >> 5, lane = t & 31, g8 = lane >> 2, tq = lane & 3;
+      const int T = (u + 7) >> 3, ntile = T * (T + 1) / 2;
+      for (int tile = warp; tile < ntile; tile += G / 32) {
+        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+        while (I * (I + 1) / 2 > tile) I--;
+        while ((I + 1) * (I + 2) / 2 <= tile) I++;
+        const int J = tile - I * (I + 1) / 2;
+        const int ra = k + 8 * I + g8, rb = k + 8 * J + g8;
+        const double* arow = F + tri(min(ra, m - 1), 0);
+        const double* brow = F + tri(min(rb, m - 1), 0);
+        const bool va = ra < m, vb = rb < m;
+        double acc[2] = {0.0, 0.0};
+        for (int kk = 0; kk < k; kk += 4) {
+          const int q = kk + tq;
+          const double av = (va && q < k) ? arow[q] * lv[q] : 0.0;
+          const double bv = (vb && q < k) ? brow[q] : 0.0;
+          dmma884(acc, av, bv);
+        }
+        const int R = k + 8 * I + g8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int Cc = k + 8 * J + 2 * tq + h;
+          if (R < m && Cc <= R) F[tri(R, Cc)] -= acc[h];
+        }
       }
     } else {
-      for (int r = c + 1 + t; r < m; r += G) {
-        double* row = F + tri(r, 0);
-        const double frc = row[c];
-        for (int s = c + 1; s <= r; s++) row[s] -= lv[s] * frc;
-        row[c] = lv[r];
+      int beg, end;
+      chunk_of((int)tri(u, 0), G, t, beg, end);
+      if (beg < end) {
+        int a = tri_row(beg), b = beg - (int)tri(a, 0);
+        for (int e = beg; e < end; e++) {
+          const double* ra = F + tri(k + a, 0);
+          const double* rb = F + tri(k + b, 0);
+          double acc = 0.0;
+          for (int q = 0; q < k; q++) acc += ra[q] * lv[q] * rb[q];
+          F[tri(k + a, k + b)] -= acc;
+          if (++b > a) { a++; b = 0; }
+        }
       }
     }
     group_sync<G>(bar);
   }
 
-  // factor slot: panel rows (lower part) + diagonal vector
+  // (4) copy-out: factor slot (panel rows, lower part, + pivots) and Schur block
   if (k > 0) {
     double* out = factors + f * L.fac_stride;
-    const int n = m * k;
-    for (int e = t; e < n; e += G) {
-      const int r = e / k, c = e - r * k;
-      if (c <= r) out[(long long)r * kp + c] = F[tri(r, c)];
+    int beg, end;
+    chunk_of(m * k, G, t, beg, end);
+    if (beg < end) {
+      int r = beg / k, c = beg - r * k;
+      for (int e = beg; e < end; e++) {
+        if (c <= r) out[(long long)r * kp + c] = F[tri(r, c)];
+        if (++c == k) { c = 0; r++; }
+      }
     }
     double* dv = out + (long long)m * kp;
     for (int c = t; c < kp; c += G) dv[c] = c < k ? F[tri(c, c)] : 0.0;
   }
-  // Schur complement, packed lower (m-k)^2
-  const int u = m - k;
   if (u > 0) {
     double* out = upd_out + f * L.upd_stride;
-    const int n = (int)tri(u, 0);
-    for (int e = t; e < n; e += G) {
-      const int a = tri_row(e), b = e - (int)tri(a, 0);
-      out[e] = F[tri(k + a, k + b)];
+    int beg, end;
+    chunk_of((int)tri(u, 0), G, t, beg, end);
+    if (beg < end) {
+      int a = tri_row(beg), b = beg - (int)tri(a, 0);
+      for (int e = beg; e < end; e++) {
+        out[e] = F[tri(k + a, k + b)];
+        if (++b > a) { a++; b = 0; }
+      }
     }
   }
 }
@@ -131,11 +205,8 @@ static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, c
                                   double* factors, double* upd_out, double thr,
                                   unsigned long long* err, cudaStream_t st) {
   const int per = small_smem_per_group(L.max_m);
-  // fronts per CTA: GPC, reduced when shared memory would not fit
-  int gpc = GPC;
-  while (gpc > 1 && (size_t)per * gpc > 200 * 1024) gpc >>= 1;
-  if (gpc != GPC) return cudaErrorInvalidConfiguration;
   const size_t smem = (size_t)per * GPC;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = factor_small_kernel<G, GPC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -154,9 +225,10 @@ cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, con
   const int mm = L.max_m;
   if (mm <= 8) return launch_small_t<4, 64>(L, child_upd, elem, factors, upd_out, thr, err, st);
   if (mm <= 16) return launch_small_t<8, 32>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 32) return launch_small_t<16, 8>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 64) return launch_small_t<32, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 128) return launch_small_t<128, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 24) return launch_small_t<16, 16>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 48) return launch_small_t<32, 8>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 80) return launch_small_t<64, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 128) return launch_small_t<128, 2>(L, child_upd, elem, factors, upd_out, thr, err, st);
   return launch_small_t<256, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
 }
 

@@ -25,6 +25,30 @@ constexpr int SB = 64;   // diagonal block rows (= factorization NB)
 constexpr int RB = 128;  // rows per CTA in the large-front row sweeps
 
 // ------------------------------------------------------------- small fronts
+// Stage the front's panel (lower part, m x k, packed to leading dimension k)
+// and its pivots d into shared memory with U loads in flight per thread.
+template <int G>
+__device__ __forceinline__ void stage_panel(double* Ls, const double* __restrict__ P, int m, int k,
+                                            int kp, int t) {
+  constexpr int U = 4;
+  const int n = m * k;
+  for (int e0 = t; e0 < n; e0 += G * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * G;
+      const int r = e / k, c = e - r * k;
+      v[u] = (e < n && c <= r) ? __ldg(P + (long long)r * kp + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * G;
+      if (e < n) Ls[e] = v[u];
+    }
+  }
+  for (int c = t; c < k; c += G) Ls[n + c] = __ldg(P + (long long)m * kp + c);
+}
+
 // Vectors: row stride ldr (total RHS columns); this launch handles columns
 // [col0, col0 + nr).  Front blocks in w_in / w_out have the same row stride.
 template <int G, int GPC>
@@ -41,7 +65,9 @@ __global__ void __launch_bounds__(G* GPC)
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
-  const double* Lp = factors + f * L.fac_stride;
+  double* Ls = W + L.max_m * nr;  // panel staged in shared memory: Ls[r*k + c], then d
+  stage_panel<G>(Ls, factors + f * L.fac_stride, m, k, kp, t);
+  const double* Lp = Ls;
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nW; e += G) {
     const int r = e / nr, j = e - r * nr;
@@ -68,11 +94,11 @@ __global__ void __launch_bounds__(G* GPC)
     const double* Wc = W + c * nr;
     for (int e = t; e < n; e += G) {
       const int r = c + 1 + e / nr, j = e % nr;
-      W[r * nr + j] -= Lp[(long long)r * kp + c] * Wc[j];
+      W[r * nr + j] -= Lp[r * k + c] * Wc[j];
     }
     group_sync<G>(bar);
   }
-  const double* dv = Lp + (long long)m * kp;
+  const double* dv = Lp + m * k;
   for (int e = t; e < nK; e += G) {
     const int r = e / nr, j = e - r * nr;
     y[(piv + r) * ldr + col0 + j] = W[e] / dv[r];
@@ -98,7 +124,9 @@ __global__ void __launch_bounds__(G* GPC)
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
-  const double* Lp = factors + f * L.fac_stride;
+  double* Ls = X + L.max_m * nr;
+  stage_panel<G>(Ls, factors + f * L.fac_stride, m, k, kp, t);
+  const double* Lp = Ls;
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nK; e += G) {
     const int r = e / nr, j = e - r * nr;
@@ -120,7 +148,7 @@ __global__ void __launch_bounds__(G* GPC)
     for (int e = t; e < nK; e += G) {
       const int c = e / nr, j = e - c * nr;
       double acc = X[e];
-      for (int r = k; r < m; r++) acc -= Lp[(long long)r * kp + c] * X[r * nr + j];
+      for (int r = k; r < m; r++) acc -= Lp[r * k + c] * X[r * nr + j];
       X[e] = acc;
     }
     group_sync<G>(bar);
@@ -130,7 +158,7 @@ __global__ void __launch_bounds__(G* GPC)
     const int n = c * nr;
     for (int e = t; e < n; e += G) {
       const int r = e / nr, j = e - r * nr;
-      X[e] -= Lp[(long long)c * kp + r] * Xc[j];
+      X[e] -= Lp[c * k + r] * Xc[j];
     }
     group_sync<G>(bar);
   }
@@ -326,7 +354,7 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
                                       const double* factors, const double* w_in,
                                       long long in_rows, double* w_out, long long out_rows,
                                       double* y, int nr, int ldr, int col0, cudaStream_t st) {
-  const int per = (int)(((size_t)L.max_m * nr * 8 + 15) & ~(size_t)15);
+  const int per = (int)(((size_t)(L.max_m * nr + L.max_m * L.max_k + L.max_m) * 8 + 15) & ~(size_t)15);
   const size_t smem = (size_t)per * GPC;
   const unsigned blocks = (unsigned)((L.n_fronts + GPC - 1) / GPC);
   if (FWD) {
@@ -346,7 +374,8 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
 }
 
 static int small_cols(const LevelArgs& L, int nrhs) {
-  const int cmax = (int)(kSmallSolveSmem / (8 * (size_t)std::max(L.max_m, 1)));
+  const long long fixed = (long long)L.max_m * L.max_k + L.max_m;
+  const int cmax = (int)((kSmallSolveSmem / 8 - fixed) / std::max(L.max_m, 1));
   return std::max(1, std::min(nrhs, cmax));
 }
 
@@ -359,7 +388,7 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
     const long long work = (long long)L.max_m * nr;
-    const long long bytes = work * 8;
+    const long long bytes = (work + (long long)L.max_m * L.max_k + L.max_m) * 8;
     cudaError_t e;
 #define TFB_SMALL(G, GPC)                                                                  \
   launch_small_solve<G, GPC, FWD>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nr, \
