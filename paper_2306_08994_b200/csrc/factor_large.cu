@@ -89,24 +89,32 @@ __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* fa
     v[j] = (r < kb && col <= r) ? Pf[(long long)(a + r) * s.kp + a + col] : (r == col ? 1.0 : 0.0);
   }
   const long long piv0 = L.piv_off[f] + a;
-  // LDL^T: a(r,s) -= (a(s,c)/d) a(r,c); column c becomes l(r,c) = a(r,c)/d
+  // LDL^T: a(r,s) -= (a(s,c)/d) a(r,c); column c becomes l(r,c) = a(r,c)/d.
+  // The pivot loop stays rolled (straight-line code executed once per CTA
+  // would miss the instruction cache); register slots are selected by
+  // compile-time indices inside the unrolled inner loops.
+#pragma unroll 1
+  for (int c = 0; c < kb; c++) {
+    double* cb = buf[c & 1];
+    const int cj = c % W;
+    const bool own = h == c / W;
+    if (own && r >= c) {
+      double vc = 0.0;
 #pragma unroll
-  for (int c = 0; c < NB; c++) {
-    if (c < kb) {
-      double* cb = buf[c & 1];
-      if (h == c / W && r >= c) cb[r] = v[c % W];
-      __syncthreads();
-      const double d = cb[c];
-      if (tid == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-      const double inv = 1.0 / d;
-      if (r > c && r < kb) {
-        const double arc = cb[r];
+      for (int j = 0; j < W; j++) vc = (j == cj) ? v[j] : vc;
+      cb[r] = vc;
+    }
+    __syncthreads();
+    const double d = cb[c];
+    if (tid == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
+    const double inv = 1.0 / d;
+    if (r > c && r < kb) {
+      const double arc = cb[r];
 #pragma unroll
-        for (int j = 0; j < W; j++) {
-          const int col = c0 + j;
-          if (col > c && col <= r) v[j] -= (cb[col] * inv) * arc;
-        }
-        if (h == c / W) v[c % W] = arc * inv;
+      for (int j = 0; j < W; j++) {
+        const int col = c0 + j;
+        if (col > c && col <= r) v[j] -= (cb[col] * inv) * arc;
+        if (own && j == cj) v[j] = arc * inv;
       }
     }
   }
@@ -116,11 +124,7 @@ __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* fa
     for (int j = 0; j < W; j++) {
       const int col = c0 + j;
       if (col <= r) Pf[(long long)(a + r) * s.kp + a + col] = v[j];
-    }
-    if (h == r / W) {
-#pragma unroll
-      for (int j = 0; j < W; j++)
-        if (c0 + j == r) Pf[(long long)s.m * s.kp + a + r] = v[j];
+      if (col == r) Pf[(long long)s.m * s.kp + a + r] = v[j];
     }
   }
   // unit-lower inverse M = L^-1, right-looking over rows t of M
@@ -128,8 +132,8 @@ __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* fa
 #pragma unroll
   for (int j = 0; j < W; j++) w[j] = (c0 + j == r) ? 1.0 : 0.0;
   __syncthreads();
-#pragma unroll
-  for (int t = 0; t < NB - 1; t++) {
+#pragma unroll 1
+  for (int t = 0; t < kb - 1; t++) {
     double* rb = buf[t & 1];
     if (r == t) {
 #pragma unroll
@@ -137,7 +141,11 @@ __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* fa
     }
     __syncthreads();
     // L[r][t] lives in the quad lane owning column block t / W
-    const double lrt = __shfl_sync(0xffffffffu, v[t % W], quad | (t / W));
+    const int tj = t % W;
+    double vt = 0.0;
+#pragma unroll
+    for (int j = 0; j < W; j++) vt = (j == tj) ? v[j] : vt;
+    const double lrt = __shfl_sync(0xffffffffu, vt, quad | (t / W));
     if (r > t && r < kb) {
 #pragma unroll
       for (int j = 0; j < W; j++)
