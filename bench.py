@@ -188,11 +188,22 @@ def run_ours(args, cfg):
            for _ in range(args.steps)]
     level_ms = np.zeros(nl)
 
+    sharded = None
+    if world > 1:
+        from paper_2306_08994_b200.distributed import ShardedFactorization, TorchComm
+        sharded = ShardedFactorization(dp, world, TorchComm(), ranks=[rank])
+
     def step(ev=None):
         record = ev is not None
-        dp.err.fill_(-1)
         if record:
             ev[0].record(stream)
+        if sharded is not None:
+            hook = (lambda L: ev[L + 1].record(stream)) if record else None
+            if sharded.factor(thr, stream, level_hook=hook) != -1:
+                raise RuntimeError("zero pivot in benchmark system")
+            sharded.solve_into(b, x, stream)
+            return
+        dp.err.fill_(-1)
         for L in range(nl):
             dp.factor_level(L, thr, sp)  # one Foata class: tf_level_factor
             if record:
@@ -202,7 +213,7 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if dp.zero_pivot_position() != -1:
+    if sharded is None and dp.zero_pivot_position() != -1:
         raise RuntimeError("zero pivot in benchmark system")
     if world > 1:
         dist.barrier()
@@ -231,21 +242,35 @@ def run_ours(args, cfg):
     x_host = torch.empty((n, nrhs), dtype=torch.float64).pin_memory()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     elem_host = torch.from_numpy(np.ascontiguousarray(fronts.values).ravel()).pin_memory()
+    def e2e_step():
+        dp.elem.copy_(elem_host, non_blocking=True)               # H2D: element matrices
+        if sharded is not None:                                   # sharded path (N > 1)
+            bd = b_host.to(dev, non_blocking=True)                # H2D: right-hand sides
+            if sharded.factor(thr, stream) != -1:
+                raise RuntimeError("zero pivot")
+            xd = torch.empty_like(bd)
+            sharded.solve_into(bd, xd, stream)
+        else:
+            fac = tf.run_sequential(plan, state)                  # public API (checks pivots)
+            xd = tf.solve(fac, b_host.to(dev, non_blocking=True))  # H2D: right-hand sides
+        x_host.copy_(xd, non_blocking=True)                       # D2H: solution
+        torch.cuda.synchronize()
+
     for _ in range(max(1, args.warmup)):
-        dp.elem.copy_(elem_host, non_blocking=True)
-        fac = tf.run_sequential(plan, state)
-        x_host.copy_(tf.solve(fac, b_host.to(dev, non_blocking=True)), non_blocking=True)
+        e2e_step()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(args.steps):
-        dp.elem.copy_(elem_host, non_blocking=True)           # H2D: element matrices
-        fac = tf.run_sequential(plan, state)                   # public API (checks pivots)
-        xd = tf.solve(fac, b_host.to(dev, non_blocking=True))  # H2D: right-hand sides
-        x_host.copy_(xd, non_blocking=True)                    # D2H: solution
-        torch.cuda.synchronize()
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
     h2d = b_host.numel() * 8 + elem_host.numel() * 8
     d2h = x_host.numel() * 8
 
@@ -277,14 +302,15 @@ def run_ours(args, cfg):
     line = {
         "metric": "factor+solve DoF/s", "value": n / (ms / 1e3), "unit": "DoF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong",  # same system for every N "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.config, "label": cfg["label"], "n_dof": n, "nrhs": nrhs,
                    "levels": nl, "factor_ms": float(level_ms.sum()),
                    "solve_ms": float(ms - level_ms.sum()),
                    "ldl_gflop": total_ldl / 1e9, "alg_bytes_gb": total_bytes / 1e9,
                    "l2": "working set >> 126 MB L2 (no flush needed)", "rel_residual": rel_res,
-                   "parallelism": f"dp{world}"},
+                   "parallelism": (f"subtree-sharded over {world} GPUs (NCCL P2P of root-ward "
+                                   f"Schur complements)" if world > 1 else "1 GPU")},
         "e2e": {"value": n / (e2e_ms / 1e3), "unit": "DoF/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms},
         "gpu_launches": launches * args.steps,

@@ -129,6 +129,8 @@ typedef struct {
   double* aux;        /* large-front levels: per front, the unit-lower inverses of its
                          64-wide diagonal blocks (ceil(k/64) x 64 x 64, row-major) */
   int64_t aux_stride; /* doubles per front in aux (tf_level_aux_doubles) */
+  int64_t front_base; /* tree index of this view's front 0 (a rank's slice; 0 = whole level) */
+  int64_t child_base; /* tree index of the front held in slot 0 of the child-level buffer */
 } tf_level_view;
 
 /* Doubles of `aux` each front of this level needs under the current

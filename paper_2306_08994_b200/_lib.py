@@ -52,6 +52,7 @@ class LevelView(C.Structure):
         ("pattern_of", C.c_void_p), ("piv_off", C.c_void_p),
         ("pat", C.c_void_p), ("maps", C.c_void_p),
         ("aux", C.c_void_p), ("aux_stride", C.c_int64),
+        ("front_base", C.c_int64), ("child_base", C.c_int64),
     ]
 
 

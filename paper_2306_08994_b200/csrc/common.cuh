@@ -36,6 +36,12 @@ struct LevelArgs {
   const int* __restrict__ maps;
   double* aux;
   long long aux_stride;
+  long long front_base;  // tree index of front 0 of this (possibly sliced) view
+  long long child_base;  // tree index of slot 0 of the child-level buffer
+  // child c of front f (slice-relative) -> slot in the child buffer / view
+  __device__ __forceinline__ long long child_slot(long long f, int c) const {
+    return 2 * (front_base + f) + c - child_base;
+  }
 };
 
 inline LevelArgs make_args(const tf_level_view* v) {
@@ -56,6 +62,8 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.maps = v->maps;
   a.aux = v->aux;
   a.aux_stride = v->aux_stride;
+  a.front_base = v->front_base;
+  a.child_base = v->child_base;
   return a;
 }
 

@@ -29,8 +29,8 @@ __global__ void large_assemble_kernel(LevelArgs L, const double* __restrict__ ch
   double* Sf = upd + f * L.upd_stride;
   const int* inv0 = L.maps + s.ioff;
   const int* inv1 = inv0 + m;
-  const double* src0 = child_upd + (2 * f) * L.child_upd_stride;
-  const double* src1 = child_upd + (2 * f + 1) * L.child_upd_stride;
+  const double* src0 = child_upd + L.child_slot(f, 0) * L.child_upd_stride;
+  const double* src1 = child_upd + L.child_slot(f, 1) * L.child_upd_stride;
   const bool two = s.nsrc == 2;
   for (long long e = blockIdx.y * (long long)blockDim.x + threadIdx.x; e < nP + nS;
        e += (long long)gridDim.y * blockDim.x) {

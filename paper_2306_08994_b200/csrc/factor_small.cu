@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(G* GPC)
           if (++b > a) { a++; b = 0; }
         }
       } else {
-        const double* src = child_upd + (2 * f + c) * L.child_upd_stride;
+        const double* src = child_upd + L.child_slot(f, c) * L.child_upd_stride;
         constexpr int U = 4;
         int e = beg;
         for (; e + U <= end; e += U) {

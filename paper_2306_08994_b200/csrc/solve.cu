@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(G* GPC)
   group_sync<G>(bar);
   if (!L.is_leaf) {
     for (int c = 0; c < s.nsrc; c++) {
-      const long long ch = 2 * f + c;
+      const long long ch = 2 * (L.front_base + f) + c - C.front_base;
       const int kc = C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
       const int len = c == 0 ? s.len0 : s.len1;
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(G* GPC)
     X[e] = y[(piv + r) * ldr + col0 + j];
   }
   if (has_parent && m > k) {
-    const long long pf = f >> 1;
-    const int c = (int)(f & 1);
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int c = (int)((L.front_base + f) & 1);
     const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
     const int* mp = PA.maps + (c == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
     const double* Xp = x_parent + pf * parent_rows * ldr + col0;
@@ -185,14 +185,14 @@ __global__ void solve_gather_fwd(LevelArgs L, LevelArgs C, const double* __restr
   const int nW = s.m * nrhs, nK = s.k * nrhs;
   int kc[2] = {0, 0};
   for (int c = 0; c < s.nsrc; c++)
-    kc[c] = C.pat[(size_t)C.pattern_of[2 * f + c] * TF_PAT_WIDTH + TF_PAT_K];
+    kc[c] = C.pat[(size_t)C.pattern_of[2 * (L.front_base + f) + c - C.front_base] * TF_PAT_WIDTH + TF_PAT_K];
   double* Wf = W + f * out_rows * nrhs;
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {
     const int r = e / nrhs, j = e - r * nrhs;
     double v = e < nK ? y[piv * nrhs + e] : 0.0;
     for (int c = 0; c < s.nsrc; c++) {
       const int i = L.maps[s.ioff + c * s.m + r];
-      if (i >= 0) v += w_child[(2 * f + c) * child_rows * nrhs + (long long)(kc[c] + i) * nrhs + j];
+      if (i >= 0) v += w_child[(2 * (L.front_base + f) + c - C.front_base) * child_rows * nrhs + (long long)(kc[c] + i) * nrhs + j];
     }
     Wf[e] = v;
   }
@@ -254,9 +254,9 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
   const int* mp = nullptr;
   const double* Xp = nullptr;
   if (has_parent) {
-    const long long pf = f >> 1;
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
     const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
-    mp = PA.maps + ((f & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    mp = PA.maps + (((L.front_base + f) & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
     Xp = x_parent + pf * parent_rows * nrhs;
   }
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {

@@ -116,14 +116,27 @@ class DevicePlan:
             self.levels.append(dl)
             child = dl.upd_stride
         self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)
-        self.factors = [torch.empty(max(1, dl.n_fronts * dl.fac_stride), dtype=torch.float64,
-                                    device=self.device) for dl in self.levels]
-        upd_max = max(dl.n_fronts * dl.upd_stride for dl in self.levels)
-        self.upd = [torch.empty(max(1, upd_max), dtype=torch.float64, device=self.device)
-                    for _ in range(2)]
+        self._factors = None  # allocated on first single-device factorization
+        self._upd = None
         self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
         self._solve_nrhs = 0
         self._blk = None
+
+    @property
+    def factors(self):
+        if self._factors is None:
+            self._factors = [torch.empty(max(1, dl.n_fronts * dl.fac_stride),
+                                         dtype=torch.float64, device=self.device)
+                             for dl in self.levels]
+        return self._factors
+
+    @property
+    def upd(self):
+        if self._upd is None:
+            upd_max = max(dl.n_fronts * dl.upd_stride for dl in self.levels)
+            self._upd = [torch.empty(max(1, upd_max), dtype=torch.float64, device=self.device)
+                         for _ in range(2)]
+        return self._upd
 
     # ---- factorization -----------------------------------------------------------
     def factor_level(self, L: int, threshold: float, sp) -> None:
