@@ -232,6 +232,20 @@ __global__ void __launch_bounds__(256) solve_fwd_block(LevelArgs L, const double
     for (int e = threadIdx.x; e < n; e += blockDim.x) y[piv * nrhs + e] = Yb[e] / dv[e / nrhs];
   }
   const int rows = min(RB, s.m - r0);
+  if (nrhs == 1) {
+    // warp per row, lanes across the 64 block columns: coalesced panel reads
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int rl = warp; rl < rows; rl += 8) {
+      const double* lrow = Lp + (long long)(r0 + rl) * s.kp + j0;
+      double acc = 0.0;
+      if (lane < kb) acc = lrow[lane] * Yb[lane];
+      if (lane + 32 < kb) acc += lrow[lane + 32] * Yb[lane + 32];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) Wf[r0 + rl] -= acc;
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) {
     const int rl = e / nrhs, j = e - rl * nrhs;
     const long long r = r0 + rl;
@@ -292,6 +306,20 @@ __global__ void __launch_bounds__(256) solve_bwd_partial(LevelArgs L, const doub
   const int rows = min(RB, s.m - r0);
   for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) sm[e] = Xf[(long long)r0 * nrhs + e];
   __syncthreads();
+  if (nrhs == 1) {
+    // 64 columns x 4 row groups, fixed-order reduction of the 4 partial sums
+    __shared__ double red[4][SB];
+    const int c = threadIdx.x & (SB - 1), g = threadIdx.x >> 6;
+    double acc = 0.0;
+    if (c < kb) {
+      const double* lcol = Lp + (long long)r0 * s.kp + j0 + c;
+      for (int q = g; q < rows; q += 4) acc += lcol[(long long)q * s.kp] * sm[q];
+    }
+    red[g][c] = acc;
+    __syncthreads();
+    if (g == 0 && c < kb) P[c] = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
+    return;
+  }
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int j = e / kb, c = e - j * kb;  // c fastest: coalesced panel reads
     const double* lcol = Lp + (long long)r0 * s.kp + j0 + c;
@@ -393,7 +421,10 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
 #define TFB_SMALL(G, GPC)                                                                  \
   launch_small_solve<G, GPC, FWD>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nr, \
                                   nrhs, col0, st)
-    if (work <= 16 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
+    if (work <= 12 && bytes * 128 <= (long long)kSmallSolveSmem) e = TFB_SMALL(1, 128);
+    else if (work <= 24 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(2, 64);
+    else if (work <= 48 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(4, 64);
+    else if (work <= 96 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
     else if (work <= 64 && bytes * 16 <= (long long)kSmallSolveSmem) e = TFB_SMALL(16, 16);
     else if (work <= 256 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
     else if (work <= 2048 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
