@@ -203,11 +203,9 @@ def run_ours(args, cfg):
                 raise RuntimeError("zero pivot in benchmark system")
             sharded.solve_into(b, x, stream)
             return
-        dp.err.fill_(-1)
-        for L in range(nl):
-            dp.factor_level(L, thr, sp)  # one Foata class: tf_level_factor
-            if record:
-                ev[L + 1].record(stream)
+        # one Foata class per level (tf_level_factor); the bottom levels as one
+        # subtree launch (tf_subtree_factor)
+        dp.factor(thr, stream, level_hook=(lambda L: ev[L + 1].record(stream)) if record else None)
         dp.solve_into(b, x, stream)
 
     for _ in range(args.warmup):

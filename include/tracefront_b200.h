@@ -156,6 +156,19 @@ int tf_level_factor(const tf_level_view* lv, const double* child_upd, const doub
                     unsigned long long* err, void* workspace, int64_t workspace_bytes,
                     void* stream);
 
+/* Bottom-level fusion: how many of the lowest levels (views[0..n_levels)) one
+ * subtree kernel can run with their intermediate Schur blocks kept in shared
+ * memory (0 or >= 2). */
+int32_t tf_subtree_fusable(const tf_level_view* views, int32_t n_levels);
+
+/* Levels 0..nlev-1 in one launch (one CTA per level-(nlev-1) subtree): same
+ * arithmetic and outputs as nlev tf_level_factor calls -- factors[L] for
+ * every fused level and the packed updates of level nlev-1 in upd_out -- but
+ * the updates between the fused levels never leave shared memory. */
+int tf_subtree_factor(const tf_level_view* views, int32_t nlev, double* const* factors,
+                      const double* elem, double* upd_out, double threshold,
+                      unsigned long long* err, void* stream);
+
 /* Forward sweep of solve (engine.py:481-487) for one level, nrhs columns,
  * row-major (n x nrhs) vectors in pivot order.  child: view of level-1 (NULL
  * at the leaves); w_child: its front blocks (stride child_rows * nrhs, update

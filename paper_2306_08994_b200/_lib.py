@@ -62,7 +62,8 @@ EXPORTS = (
     "tf_plan_level", "tf_plan_pivot_order", "tf_plan_node_lists", "tf_plan_node_lists_len",
     "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
     "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
-    "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_build_info",
+    "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_subtree_fusable",
+    "tf_subtree_factor", "tf_build_info",
 )
 
 _lib = None
@@ -118,6 +119,10 @@ def load() -> C.CDLL:
     lib.tf_level_launch_count.restype = i32
     lib.tf_set_small_max_m.argtypes = [i32]
     lib.tf_set_small_max_m.restype = i32
+    lib.tf_subtree_fusable.argtypes = [vp, i32]
+    lib.tf_subtree_fusable.restype = i32
+    lib.tf_subtree_factor.argtypes = [vp, i32, vp, vp, vp, C.c_double, vp, vp]
+    lib.tf_subtree_factor.restype = C.c_int
     lib.tf_build_info.argtypes = []
     lib.tf_build_info.restype = C.c_char_p
     _lib = lib

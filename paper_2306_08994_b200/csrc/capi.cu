@@ -20,6 +20,10 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,
                                 int nrhs, int scatter, cudaStream_t st);
 long long solve_workspace_doubles(const LevelArgs& L, int nrhs);
+int subtree_fusable_levels(const LevelArgs* lv, int n_levels);
+cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* fac,
+                                  const double* elem, double* upd_out, double thr,
+                                  unsigned long long* err, cudaStream_t st);
 int large_panel_launches(int max_k);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
 int g_small_max_m = 112;  // measured best split on B200 (tools/sweep.sh)
@@ -65,6 +69,27 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
   if (lv->max_k > 0 && (!lv->aux || lv->aux_stride < large_aux_doubles(lv->max_k)))
     return TF_ERR_INVALID;
   return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, st));
+}
+
+extern "C" int32_t tf_subtree_fusable(const tf_level_view* views, int32_t n_levels) {
+  if (!views || n_levels < 1) return 0;
+  LevelArgs lv[16];
+  const int n = n_levels < 16 ? n_levels : 16;
+  for (int L = 0; L < n; L++) lv[L] = make_args(&views[L]);
+  return subtree_fusable_levels(lv, n);
+}
+
+extern "C" int tf_subtree_factor(const tf_level_view* views, int32_t nlev,
+                                 double* const* factors, const double* elem, double* upd_out,
+                                 double threshold, unsigned long long* err, void* stream) {
+  if (!views || !factors || !elem || !err || nlev < 1 || nlev > 10) return TF_ERR_INVALID;
+  LevelArgs lv[10];
+  for (int L = 0; L < nlev; L++) {
+    lv[L] = make_args(&views[L]);
+    if (level_is_large(lv[L].is_leaf, lv[L].max_m) || lv[L].front_base != 0) return TF_ERR_INVALID;
+  }
+  return status(launch_factor_subtree(lv, nlev, factors, elem, upd_out, threshold, err,
+                                      (cudaStream_t)stream));
 }
 
 extern "C" int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,

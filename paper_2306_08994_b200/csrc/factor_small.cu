@@ -24,6 +24,8 @@
 
 namespace tfb {
 
+int small_smem_per_group(int max_m);
+
 // Thread t's contiguous chunk [beg, end) of n items split over G threads.
 __device__ __forceinline__ void chunk_of(int n, int G, int t, int& beg, int& end) {
   const int c = (n + G - 1) / G;
@@ -31,25 +33,16 @@ __device__ __forceinline__ void chunk_of(int n, int G, int t, int& beg, int& end
   end = min(n, beg + c);
 }
 
-template <int G, int GPC>
-__global__ void __launch_bounds__(G* GPC)
-    factor_small_kernel(LevelArgs L, const double* __restrict__ child_upd,
-                        const double* __restrict__ elem, double* __restrict__ factors,
-                        double* __restrict__ upd_out, double threshold,
-                        unsigned long long* err, int smem_per_group) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int gid = threadIdx.x / G;
-  const int t = threadIdx.x - gid * G;
-  const int bar = 1 + gid;
-  const long long f = (long long)blockIdx.x * GPC + gid;
-  if (f >= L.n_fronts) return;  // whole group exits; syncs are group-local
-  unsigned char* my = smem_raw + (size_t)gid * smem_per_group;
-  const int mm = L.max_m;
-  double* F = reinterpret_cast<double*>(my);
-  double* lv = F + tri(mm, 0);
-  int* mp = reinterpret_cast<int*>(lv + mm);
-
-  const Shape S = front_shape(L, f);
+// One front, one thread group: extend-add of src0/src1 (packed child Schur
+// blocks, or the element matrix at the leaves), partial LDL^T, Schur block,
+// copy-out of the factor slot and of the packed update to upd_dst.
+template <int G>
+__device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, const Shape& S,
+                                             const double* __restrict__ src0,
+                                             const double* __restrict__ src1, double* F,
+                                             double* lv, int* mp, double* __restrict__ fac_out,
+                                             double* __restrict__ upd_dst, double threshold,
+                                             unsigned long long* err, int t, int bar) {
   const int m = S.m, k = S.k, kp = S.kp, u = m - k;
   const int nF = (int)tri(m, 0);
 
@@ -68,20 +61,20 @@ __global__ void __launch_bounds__(G* GPC)
     if (beg < end) {
       int a = tri_row(beg), b = beg - (int)tri(a, 0);
       if (L.is_leaf) {
-        const double* E = elem + f * L.elem_stride;
+        const double* E = src0;
         for (int e = beg; e < end; e++) {
           const int R = cm[a], C = cm[b];
           F[R > C ? tri(R, C) : tri(C, R)] += E[a * L.elem_ld + b];
           if (++b > a) { a++; b = 0; }
         }
       } else {
-        const double* src = child_upd + L.child_slot(f, c) * L.child_upd_stride;
+        const double* src = c == 0 ? src0 : src1;
         constexpr int U = 4;
         int e = beg;
         for (; e + U <= end; e += U) {
           double v[U];
 #pragma unroll
-          for (int q = 0; q < U; q++) v[q] = __ldg(src + e + q);
+          for (int q = 0; q < U; q++) v[q] = src[e + q];
 #pragma unroll
           for (int q = 0; q < U; q++) {
             const int R = cm[a], C = cm[b];
@@ -91,7 +84,7 @@ __global__ void __launch_bounds__(G* GPC)
         }
         for (; e < end; e++) {
           const int R = cm[a], C = cm[b];
-          F[R > C ? tri(R, C) : tri(C, R)] += __ldg(src + e);
+          F[R > C ? tri(R, C) : tri(C, R)] += src[e];
           if (++b > a) { a++; b = 0; }
         }
       }
@@ -166,31 +159,52 @@ __global__ void __launch_bounds__(G* GPC)
 
   // (4) copy-out: factor slot (panel rows, lower part, + pivots) and Schur block
   if (k > 0) {
-    double* out = factors + f * L.fac_stride;
     int beg, end;
     chunk_of(m * k, G, t, beg, end);
     if (beg < end) {
       int r = beg / k, c = beg - r * k;
       for (int e = beg; e < end; e++) {
-        if (c <= r) out[(long long)r * kp + c] = F[tri(r, c)];
+        if (c <= r) fac_out[(long long)r * kp + c] = F[tri(r, c)];
         if (++c == k) { c = 0; r++; }
       }
     }
-    double* dv = out + (long long)m * kp;
+    double* dv = fac_out + (long long)m * kp;
     for (int c = t; c < kp; c += G) dv[c] = c < k ? F[tri(c, c)] : 0.0;
   }
   if (u > 0) {
-    double* out = upd_out + f * L.upd_stride;
     int beg, end;
     chunk_of((int)tri(u, 0), G, t, beg, end);
     if (beg < end) {
       int a = tri_row(beg), b = beg - (int)tri(a, 0);
       for (int e = beg; e < end; e++) {
-        out[e] = F[tri(k + a, k + b)];
+        upd_dst[e] = F[tri(k + a, k + b)];
         if (++b > a) { a++; b = 0; }
       }
     }
   }
+}
+
+template <int G, int GPC>
+__global__ void __launch_bounds__(G* GPC)
+    factor_small_kernel(LevelArgs L, const double* __restrict__ child_upd,
+                        const double* __restrict__ elem, double* __restrict__ factors,
+                        double* __restrict__ upd_out, double threshold,
+                        unsigned long long* err, int smem_per_group) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int gid = threadIdx.x / G;
+  const int t = threadIdx.x - gid * G;
+  const long long f = (long long)blockIdx.x * GPC + gid;
+  if (f >= L.n_fronts) return;  // whole group exits; syncs are group-local
+  unsigned char* my = smem_raw + (size_t)gid * smem_per_group;
+  double* F = reinterpret_cast<double*>(my);
+  double* lv = F + tri(L.max_m, 0);
+  int* mp = reinterpret_cast<int*>(lv + L.max_m);
+  const Shape S = front_shape(L, f);
+  const double* s0 = L.is_leaf ? elem + f * L.elem_stride
+                               : child_upd + L.child_slot(f, 0) * L.child_upd_stride;
+  const double* s1 = L.is_leaf ? nullptr : child_upd + L.child_slot(f, 1) * L.child_upd_stride;
+  factor_front<G>(L, f, S, s0, s1, F, lv, mp, factors + f * L.fac_stride,
+                  upd_out + f * L.upd_stride, threshold, err, t, 1 + gid);
 }
 
 int small_smem_per_group(int max_m) {
@@ -230,6 +244,112 @@ cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, con
   if (mm <= 80) return launch_small_t<64, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
   if (mm <= 128) return launch_small_t<128, 2>(L, child_upd, elem, factors, upd_out, thr, err, st);
   return launch_small_t<256, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
+}
+
+// ---------------------------------------------------------------- subtrees
+// Levels 0..S-1 fused: each thread group (G = 8 threads) owns one subtree,
+// rooted at a level-(S-1) front, and factors its fronts level by level; the
+// packed updates between the fused levels stay in the group's shared-memory
+// arenas, so only the factor slots and the level-(S-1) updates reach HBM.
+// 32 groups per CTA keep many independent subtrees in flight per SM.
+constexpr int kMaxFuse = 10;
+constexpr int kSubG = 8, kSubNG = 32;
+struct SubtreeArgs {
+  int nlev;
+  int arena_doubles[2];  // per group
+  int ws_bytes;          // per group
+  LevelArgs lv[kMaxFuse];
+  double* fac[kMaxFuse];
+};
+
+__global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
+    SubtreeArgs A, const double* __restrict__ elem, double* __restrict__ upd_out,
+    double threshold, unsigned long long* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int gid = threadIdx.x / kSubG, t = threadIdx.x - gid * kSubG;
+  const int top = A.nlev - 1;
+  const long long root = (long long)blockIdx.x * kSubNG + gid;
+  if (root >= A.lv[top].n_fronts) return;  // group-local exit
+  const size_t per = sizeof(double) * (A.arena_doubles[0] + A.arena_doubles[1]) + A.ws_bytes;
+  unsigned char* mine = smem_raw + (size_t)gid * per;
+  double* arena[2] = {reinterpret_cast<double*>(mine),
+                      reinterpret_cast<double*>(mine) + A.arena_doubles[0]};
+  unsigned char* ws = mine + sizeof(double) * (A.arena_doubles[0] + A.arena_doubles[1]);
+  for (int L = 0; L < A.nlev; L++) {
+    const LevelArgs& lv = A.lv[L];
+    double* F = reinterpret_cast<double*>(ws);
+    double* lvec = F + tri(lv.max_m, 0);
+    int* mp = reinterpret_cast<int*>(lvec + lv.max_m);
+    double* prev = arena[(L + 1) & 1];
+    double* cur = arena[L & 1];
+    const int cst = L > 0 ? (int)tri(A.lv[L - 1].max_upd, 0) : 0;
+    const int ost = (int)tri(lv.max_upd, 0);
+    const long long base = root << (top - L);
+    const long long cnt = min((long long)1 << (top - L), (long long)lv.n_fronts - base);
+    for (long long i = 0; i < cnt; i++) {
+      const long long f = base + i;
+      const Shape S = front_shape(lv, f);
+      const double* s0 = lv.is_leaf ? elem + f * lv.elem_stride : prev + (2 * i) * cst;
+      const double* s1 = lv.is_leaf ? nullptr : prev + (2 * i + 1) * cst;
+      double* dst = L == top ? upd_out + f * lv.upd_stride : cur + i * ost;
+      factor_front<kSubG>(lv, f, S, s0, s1, F, lvec, mp, A.fac[L] + f * lv.fac_stride, dst,
+                          threshold, err, t, 0);
+      group_sync<kSubG>(0);
+    }
+  }
+}
+
+// Shared-memory plan of one subtree group; 0 when the levels cannot be fused.
+static size_t subtree_group_bytes(const LevelArgs* lv, int nlev, int arena[2], int* ws) {
+  int mm = 1;
+  arena[0] = arena[1] = 0;
+  for (int L = 0; L < nlev; L++) {
+    mm = std::max(mm, lv[L].max_m);
+    if (L < nlev - 1) {
+      const int nf = 1 << (nlev - 1 - L);
+      arena[L & 1] = std::max(arena[L & 1], nf * (int)tri(lv[L].max_upd, 0));
+    }
+  }
+  arena[0] = (arena[0] + 1) & ~1;
+  arena[1] = (arena[1] + 1) & ~1;
+  *ws = small_smem_per_group(mm);
+  return sizeof(double) * (arena[0] + arena[1]) + *ws;
+}
+
+int subtree_fusable_levels(const LevelArgs* lv, int n_levels) {
+  int best = 0;
+  for (int S = 2; S <= std::min(n_levels, kMaxFuse); S++) {
+    bool ok = true;
+    for (int L = 0; L < S; L++)
+      ok = ok && lv[L].max_m <= 16 && !level_is_large(lv[L].is_leaf, lv[L].max_m);
+    if (!ok) break;
+    int ar[2], ws;
+    if (subtree_group_bytes(lv, S, ar, &ws) * kSubNG > 200 * 1024) break;
+    best = S;
+  }
+  return best;
+}
+
+cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* fac,
+                                  const double* elem, double* upd_out, double thr,
+                                  unsigned long long* err, cudaStream_t st) {
+  if (nlev < 1 || nlev > kMaxFuse) return cudaErrorInvalidValue;
+  SubtreeArgs A;
+  A.nlev = nlev;
+  for (int L = 0; L < nlev; L++) {
+    A.lv[L] = lv[L];
+    A.fac[L] = fac[L];
+  }
+  const size_t per = subtree_group_bytes(lv, nlev, A.arena_doubles, &A.ws_bytes);
+  const size_t smem = per * kSubNG;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(factor_subtree_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long roots = lv[nlev - 1].n_fronts;
+  const unsigned blocks = (unsigned)((roots + kSubNG - 1) / kSubNG);
+  factor_subtree_kernel<<<blocks, kSubG * kSubNG, smem, st>>>(A, elem, upd_out, thr, err);
+  return cudaGetLastError();
 }
 
 }  // namespace tfb

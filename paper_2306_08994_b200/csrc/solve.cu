@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(256) solve_fwd_block(LevelArgs L, const double
   extern __shared__ __align__(16) double sm[];
   double* Wb = sm;                 // [SB][nrhs] right-hand block
   double* Yb = sm + SB * nrhs;     // [SB][nrhs] solved block
+  double* Ms = Yb + SB * nrhs;     // [SB][SB] diagonal-block inverse
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(j0 + SB, s.k) - j0;
@@ -217,10 +218,12 @@ __global__ void __launch_bounds__(256) solve_fwd_block(LevelArgs L, const double
   double* Wf = W + f * out_rows * nrhs;
   const int n = kb * nrhs;
   for (int e = threadIdx.x; e < n; e += blockDim.x) Wb[e] = Wf[(long long)j0 * nrhs + e];
+#pragma unroll 4
+  for (int e = threadIdx.x; e < SB * SB; e += blockDim.x) Ms[e] = __ldg(M + e);
   __syncthreads();
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int r = e / nrhs, j = e - r * nrhs;
-    const double* mr = M + r * SB;
+    const double* mr = Ms + r * SB;
     double acc = Wb[e];  // M has a unit diagonal
     for (int q = 0; q < r; q++) acc += mr[q] * Wb[q * nrhs + j];
     Yb[e] = acc;
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(256) solve_bwd_block(LevelArgs L, double* X, l
                                                         double* y, int nrhs, int j0,
                                                         const double* __restrict__ partial,
                                                         int nchunk) {
-  extern __shared__ __align__(16) double sm[];  // Rb [SB][nrhs]
+  extern __shared__ __align__(16) double sm[];  // Rb [SB][nrhs], then M [SB][SB]
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(j0 + SB, s.k) - j0;
@@ -344,6 +347,9 @@ __global__ void __launch_bounds__(256) solve_bwd_block(LevelArgs L, double* X, l
   const double* M = L.aux + f * L.aux_stride + (long long)(j0 / SB) * SB * SB;
   double* Xf = X + f * out_rows * nrhs;
   const int n = kb * nrhs;
+  double* Ms = sm + SB * nrhs;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < SB * SB; e += blockDim.x) Ms[e] = __ldg(M + e);
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     double v = Xf[(long long)j0 * nrhs + e];
     for (int x = 0; x < used; x++) v -= partial[((f * nchunk + x) * SB) * (long long)nrhs + e];
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(256) solve_bwd_block(LevelArgs L, double* X, l
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int c = e / nrhs, j = e - c * nrhs;
     double acc = sm[e];  // (M^T)[c][c] = 1
-    for (int q = c + 1; q < kb; q++) acc += M[q * SB + c] * sm[q * nrhs + j];
+    for (int q = c + 1; q < kb; q++) acc += Ms[q * SB + c] * sm[q * nrhs + j];
     Xf[(long long)j0 * nrhs + e] = acc;
     y[piv * nrhs + e] = acc;
   }
@@ -451,7 +457,7 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
   const long long nW = (long long)L.max_m * nrhs;
   solve_gather_fwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, C, w_child, child_rows, w_out, out_rows, y, nrhs);
-  const size_t smem = sizeof(double) * 2 * SB * (size_t)nrhs;
+  const size_t smem = sizeof(double) * (2 * SB * (size_t)nrhs + SB * SB);
   cudaFuncSetAttribute(solve_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int j0 = 0; j0 < L.max_k; j0 += SB) {
     const int rows = std::max(1, L.max_m - j0 - 1);
@@ -475,7 +481,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
                      st>>>(L, PA, has_parent, x_parent, parent_rows, x_out, out_rows, y, nrhs);
   const int nchunk = (L.max_m + RB - 1) / RB;
   const size_t smp = sizeof(double) * RB * (size_t)nrhs;
-  const size_t smb = sizeof(double) * SB * (size_t)nrhs;
+  const size_t smb = sizeof(double) * (SB * (size_t)nrhs + SB * SB);
   cudaFuncSetAttribute(solve_bwd_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
   cudaFuncSetAttribute(solve_bwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
   const int nblk = (L.max_k + SB - 1) / SB;

@@ -18,12 +18,19 @@ Device memory layout per level L (all float64, row-major):
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
 import torch
 
 from . import _lib
+
+
+# Bottom-level subtree fusion is implemented and parity-tested but measured
+# slower than the per-level kernels on B200 (tools/fuse_sweep.sh), so it is off
+# unless a cap is set.
+FUSE_CAP_DEFAULT = 0
 
 
 def _tri(n):
@@ -121,6 +128,8 @@ class DevicePlan:
         self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
         self._solve_nrhs = 0
         self._blk = None
+        self.fuse_bottom = True  # run the lowest levels as one subtree kernel when possible
+        self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
     @property
     def factors(self):
@@ -147,13 +156,42 @@ class DevicePlan:
                                       C.c_double(threshold), _ptr(self.err), None, 0, sp)
         _lib.check(rc, f"tf_level_factor(level {L})")
 
-    def factor(self, threshold: float, stream: Optional[torch.cuda.Stream] = None) -> None:
-        """Enqueue every level on `stream`; no host synchronisation."""
+    @property
+    def fused_levels(self) -> int:
+        """Bottom levels run as one subtree launch (0: off; tf_subtree_fusable)."""
+        if not self.fuse_bottom:
+            return 0
+        arr = (_lib.LevelView * len(self.levels))(*[dl.view for dl in self.levels])
+        n = int(self.lib.tf_subtree_fusable(C.cast(arr, C.c_void_p), len(self.levels)))
+        cap = int(os.environ.get("TFB_FUSE_LEVELS", str(self.fuse_cap)))
+        n = min(n, cap)
+        return n if n >= 2 else 0
+
+    def factor(self, threshold: float, stream: Optional[torch.cuda.Stream] = None,
+               level_hook=None) -> None:
+        """Enqueue every level on `stream`; no host synchronisation.
+
+        level_hook(L), if given, runs after the launches that complete level L
+        (fused bottom levels complete together)."""
         st = stream or torch.cuda.current_stream(self.device)
         sp = C.c_void_p(st.cuda_stream)
         self.err.fill_(-1)
-        for L in range(len(self.levels)):
+        nf = self.fused_levels
+        if nf >= 2:
+            views = (_lib.LevelView * nf)(*[dl.view for dl in self.levels[:nf]])
+            facs = (C.c_void_p * nf)(*[self.factors[L].data_ptr() for L in range(nf)])
+            rc = self.lib.tf_subtree_factor(C.cast(views, C.c_void_p), nf,
+                                            C.cast(facs, C.c_void_p), _ptr(self.elem),
+                                            _ptr(self.upd[(nf - 1) & 1]), C.c_double(threshold),
+                                            _ptr(self.err), sp)
+            _lib.check(rc, f"tf_subtree_factor(levels 0..{nf - 1})")
+            if level_hook is not None:
+                for L in range(nf):
+                    level_hook(L)
+        for L in range(max(nf, 0) if nf >= 2 else 0, len(self.levels)):
             self.factor_level(L, threshold, sp)
+            if level_hook is not None:
+                level_hook(L)
 
     def zero_pivot_position(self) -> int:
         """-1, or the pivot-order position of the earliest pivot at/below threshold."""

@@ -29,6 +29,7 @@ from .device import DevicePlan, require_cuda
 from .errors import ZeroPivotError
 
 ZERO_PIVOT_RELATIVE = 1e-14  # engine.py:35
+FUSE_BOTTOM = True  # run the lowest tree levels as one subtree launch when they fit
 
 
 @dataclass
@@ -49,6 +50,7 @@ def init_state(system, plan, debug: bool = False) -> ExecState:
 def compile_execution(plan, schedule=None, state: Optional[ExecState] = None) -> DevicePlan:
     """Upload the level tables once; reusable across factorizations (engine.py:335-344)."""
     dp = DevicePlan(plan, plan.tree.fronts)
+    dp.fuse_bottom = FUSE_BOTTOM
     if state is not None:
         state.compiled = dp
     return dp

@@ -30,14 +30,17 @@ def normwise(keys, vals, d):
     return np.abs(got - vals).max() / np.abs(vals).max()
 
 
-@pytest.fixture(params=["smem", "large"])
+@pytest.fixture(params=["smem", "large", "fused"])
 def front_path(request, cuda_ok):
-    """Run with the default shared-memory kernels, or force every non-leaf level
-    through the blocked large-front (DMMA) kernels."""
-    from paper_2306_08994_b200.device import set_small_front_limit
-    old = set_small_front_limit(232 if request.param == "smem" else 1)
+    """Shared-memory fronts up to m=232; every non-leaf level forced through the
+    blocked large-front (DMMA) kernels; or the bottom levels fused into
+    subtree launches (tf_subtree_factor)."""
+    from paper_2306_08994_b200 import device
+    old = device.set_small_front_limit(1 if request.param == "large" else 232)
+    device.FUSE_CAP_DEFAULT = 10 if request.param == "fused" else 0
     yield request.param
-    set_small_front_limit(old)
+    device.FUSE_CAP_DEFAULT = 0
+    device.set_small_front_limit(old)
 
 
 @pytest.mark.gpu

@@ -61,3 +61,46 @@ print(f"solve nrhs={a.nrhs} {ts:.3f} ms")
 r = torch.from_numpy(system.matvec(x.cpu().numpy())).cuda() - b
 print("rel residual", (r.abs().max() / b.abs().max()).item())
 print(json.dumps({"factor_ms": tot, "solve_ms": ts, "dof_per_s": mesh.n_dof / (tot + ts) * 1e3}))
+
+# ---- per-level solve timing (forward then backward), CUDA events between launches
+def solve_levels(nrhs):
+    bb = torch.randn(mesh.n_dof, nrhs, dtype=torch.float64, device="cuda")
+    xx = torch.empty_like(bb)
+    dp.solve_into(bb, xx)  # allocate blocks
+    torch.cuda.synchronize()
+    nl = len(dp.levels)
+    evf = [torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)]
+    evb = [torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)]
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+    blk, y = dp._blk, dp._y
+    lib.tf_permute_rows(P(dp.pivot_order), dp.n_pivots, P(bb), P(y), nrhs, 0, sp)
+    prev = None
+    evf[0].record()
+    for L, dl in enumerate(dp.levels):
+        cur = blk[L & 1]
+        ch = dp.levels[L - 1] if L > 0 else None
+        assert lib.tf_level_solve_fwd(C.byref(dl.view), C.byref(ch.view) if ch else None,
+                                      P(dp.factors[L]), P(prev), ch.max_m if ch else 0, P(cur),
+                                      dl.max_m, P(y), nrhs, sp) == 0
+        prev = cur
+        evf[L + 1].record()
+    prev = None
+    evb[nl].record()
+    for L in range(nl - 1, -1, -1):
+        dl = dp.levels[L]
+        cur = blk[L & 1]
+        pa = dp.levels[L + 1] if L + 1 < nl else None
+        assert lib.tf_level_solve_bwd(C.byref(dl.view), C.byref(pa.view) if pa else None,
+                                      P(dp.factors[L]), P(prev), pa.max_m if pa else 0, P(cur),
+                                      dl.max_m, P(y), nrhs, P(dp._ws), dp._ws_bytes, sp) == 0
+        prev = cur
+        evb[L].record()
+    torch.cuda.synchronize()
+    fw = [evf[L].elapsed_time(evf[L + 1]) for L in range(nl)]
+    bw = [evb[L + 1].elapsed_time(evb[L]) for L in range(nl)]
+    print(f"solve nrhs={nrhs} fwd {sum(fw):.3f} ms bwd {sum(bw):.3f} ms")
+    for L in range(nl):
+        print(f"  L{L:2d} fwd {fw[L]:8.3f} bwd {bw[L]:8.3f} ms")
+
+solve_levels(a.nrhs)
