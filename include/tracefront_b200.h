@@ -131,6 +131,8 @@ typedef struct {
   int64_t aux_stride; /* doubles per front in aux (tf_level_aux_doubles) */
   int64_t front_base; /* tree index of this view's front 0 (a rank's slice; 0 = whole level) */
   int64_t child_base; /* tree index of the front held in slot 0 of the child-level buffer */
+  int64_t level_fronts; /* fronts of the whole level (a slice keeps the full count, so every
+                           rank picks the same kernel variants) */
 } tf_level_view;
 
 /* Doubles of `aux` each front of this level needs under the current

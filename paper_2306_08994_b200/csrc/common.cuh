@@ -38,6 +38,7 @@ struct LevelArgs {
   long long aux_stride;
   long long front_base;  // tree index of front 0 of this (possibly sliced) view
   long long child_base;  // tree index of slot 0 of the child-level buffer
+  long long level_fronts;  // fronts of the whole level (variant choices use this)
   // child c of front f (slice-relative) -> slot in the child buffer / view
   __device__ __forceinline__ long long child_slot(long long f, int c) const {
     return 2 * (front_base + f) + c - child_base;
@@ -64,6 +65,7 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.aux_stride = v->aux_stride;
   a.front_base = v->front_base;
   a.child_base = v->child_base;
+  a.level_fronts = v->level_fronts > 0 ? v->level_fronts : v->n_fronts;
   return a;
 }
 

@@ -152,9 +152,196 @@ __global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* fa
         if (c0 + j <= t) w[j] -= lrt * rb[c0 + j];
     }
   }
+  // aux block: strict lower = M, diagonal = d, strict upper = l transposed
   double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
 #pragma unroll
-  for (int j = 0; j < W; j++) M[r * NB + c0 + j] = w[j];
+  for (int j = 0; j < W; j++) {
+    const int col = c0 + j;
+    if (col < r) {
+      M[r * NB + col] = w[j];
+      M[col * NB + r] = r < kb ? v[j] : 0.0;
+    } else if (col == r) {
+      M[r * NB + r] = r < kb ? v[j] : 1.0;
+    }
+  }
+}
+
+// One 64-wide diagonal block of every front's panel, fused with the triangular
+// solve of the rows below it.  grid = (fronts, row tiles of 64).  Every CTA
+// factors the diagonal block redundantly in shared memory (blocked LDL^T:
+// 16-column panels with rank-1 steps, DMMA rank-16 trailing updates), forms
+// its unit-lower inverse M (inverted 16x16 diagonal blocks + block
+// substitution), then solves its 64-row tile as a DMMA product
+// P_rb <- (P_rb M^T) D^-1.  The CTA of row tile 0 also writes l, d and M.
+constexpr int TRB = 64;
+constexpr int kFusedBlockMaxFronts = 2;
+constexpr int DLD = NB + 1, ALD = NB + 4;
+constexpr size_t kBlockSmem = sizeof(double) * (2 * NB * DLD + TRB * ALD + 2 * NB);
+
+__global__ void __launch_bounds__(256) large_block_kernel(LevelArgs L, double* factors, int a,
+                                                           double threshold,
+                                                           unsigned long long* err) {
+  extern __shared__ __align__(16) double bsm[];
+  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(bsm);
+  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(bsm + NB * DLD);
+  double(*At)[ALD] = reinterpret_cast<double(*)[ALD]>(bsm + 2 * NB * DLD);
+  double* dv = bsm + 2 * NB * DLD + TRB * ALD;
+  double* lv = dv + NB;
+  const long long f = blockIdx.x;
+  const Shape s = front_shape(L, f);
+  const int kb = min(a + NB, s.k) - a;
+  if (kb <= 0) return;
+  const int row0 = a + kb + blockIdx.y * TRB;
+  const bool writer = blockIdx.y == 0;
+  if (!writer && row0 >= s.m) return;
+  const int rows = min(TRB, s.m - row0);
+  double* Pf = factors + f * L.fac_stride;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, tq = lane & 3;
+
+  // 1. diagonal block (identity pad beyond kb) and this CTA's row tile
+  for (int e = tid; e < NB * NB; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    D[i][j] = (i < kb && j <= i) ? Pf[(long long)(a + i) * s.kp + a + j] : (i == j ? 1.0 : 0.0);
+    At[i][j] = (i < rows && j < kb) ? Pf[(long long)(row0 + i) * s.kp + a + j] : 0.0;
+  }
+  __syncthreads();
+
+  // 2. blocked LDL^T of D
+  const long long piv0 = L.piv_off[f] + a;
+  for (int c0 = 0; c0 < kb; c0 += 16) {
+    const int c1 = min(c0 + 16, kb);
+    for (int c = c0; c < c1; c++) {
+      const double d = D[c][c];
+      if (writer && tid == 0 && fabs(d) <= threshold)
+        record_zero_pivot(err, (unsigned long long)(piv0 + c));
+      if (tid > c && tid < NB) {
+        const double l = D[tid][c] / d;
+        lv[tid] = l;
+        D[tid][c] = l;
+      }
+      if (tid == c) dv[c] = d;
+      __syncthreads();
+      const int nc = c1 - c - 1;
+      if (nc > 0) {
+        const int n = (NB - c - 1) * nc;
+        for (int e = tid; e < n; e += 256) {
+          const int r = c + 1 + e / nc, q = c + 1 + e % nc;
+          if (q <= r) D[r][q] -= lv[q] * (lv[r] * d);
+        }
+      }
+      __syncthreads();
+    }
+    // rank-(c1-c0) DMMA update of the trailing columns [c0+16, 64)
+    const int t0 = c0 + 16;
+    if (t0 < NB) {
+      const int T = (NB - t0) >> 3, ntile = T * (T + 1) / 2;
+      for (int tile = warp; tile < ntile; tile += 8) {
+        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+        while (I * (I + 1) / 2 > tile) I--;
+        while ((I + 1) * (I + 2) / 2 <= tile) I++;
+        const int J = tile - I * (I + 1) / 2;
+        const int ra = t0 + 8 * I + g8, rb = t0 + 8 * J + g8;
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4) {
+          const int q = c0 + kk + tq;
+          const bool v = q < c1;
+          dmma884(acc, v ? D[ra][q] * dv[q] : 0.0, v ? D[rb][q] : 0.0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cc = t0 + 8 * J + 2 * tq + h;
+          if (cc <= ra) D[ra][cc] -= acc[h];
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // 3. M = L^-1: 16x16 diagonal blocks (warp w < 4, lane c < 16 owns column c) ...
+  if (warp < 4 && lane < 16) {
+    const int o = warp * 16, c = lane;
+    for (int r = 0; r < 16; r++) Mi[o + r][o + c] = r == c ? 1.0 : 0.0;
+    for (int r = c + 1; r < 16; r++) {
+      double acc = 0.0;
+      for (int t = c; t < r; t++) acc -= D[o + r][o + t] * Mi[o + t][o + c];
+      Mi[o + r][o + c] = acc;
+    }
+  }
+  __syncthreads();
+  // ... then block rows: M_ij = -M_ii * sum_{t=j}^{i-1} L_it M_tj
+  for (int bi = 1; bi < 4; bi++) {
+    const int oi = 16 * bi;
+    // S_ij into lv-free scratch: reuse At? no -- use the upper triangle of Mi as scratch
+    for (int e = tid; e < bi * 256; e += 256) {
+      const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int oj = 16 * bj;
+      double acc = 0.0;
+      for (int t = oj; t < oi; t++) acc += D[oi + r][t] * Mi[t][oj + c];
+      Mi[oj + c][oi + r] = acc;  // scratch: upper part, transposed
+    }
+    __syncthreads();
+    for (int e = tid; e < bi * 256; e += 256) {
+      const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int oj = 16 * bj;
+      double acc = 0.0;
+      for (int t = 0; t <= r; t++) acc -= Mi[oi + r][oi + t] * Mi[oj + c][oi + t];
+      Mi[oi + r][oj + c] = acc;
+    }
+    __syncthreads();
+  }
+  // clear the scratch (upper part) so M is exactly lower-triangular
+  for (int e = tid; e < NB * NB; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    if (j > i) Mi[i][j] = 0.0;
+  }
+  __syncthreads();
+
+  // 4. write d and the aux block: strict lower = M, diagonal = d, strict upper =
+  // l transposed.  The panel's own diagonal block is not rewritten here: other
+  // CTAs of this launch may still be reading its assembled values, so
+  // large_diag_finalize_kernel copies l, d into it after the level.
+  if (writer) {
+    for (int c = tid; c < kb; c += 256) Pf[(long long)s.m * s.kp + a + c] = dv[c];
+    double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int i = e >> 6, j = e & 63;
+      M[e] = j < i ? Mi[i][j] : (j == i ? (i < kb ? dv[i] : 1.0) : (j < kb ? D[j][i] : 0.0));
+    }
+  }
+
+  // 5. row tile: X = At M^T, then column c / d_c (DMMA, 8 tiles of 8x8 per warp)
+  if (rows > 0) {
+    for (int tile = warp; tile < 64; tile += 8) {
+      const int I = tile >> 3, J = tile & 7;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll 4
+      for (int kk = 0; kk < NB; kk += 4)
+        dmma884(acc, At[8 * I + g8][kk + tq], Mi[8 * J + g8][kk + tq]);
+      const int r = 8 * I + g8;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = 8 * J + 2 * tq + h;
+        if (r < rows && c < kb) Pf[(long long)(row0 + r) * s.kp + a + c] = acc[h] / dv[c];
+      }
+    }
+  }
+}
+
+// Copy every diagonal block's l (aux strict upper, transposed) and d into the
+// panel once the level's launches no longer read the assembled values.
+__global__ void large_diag_finalize_kernel(LevelArgs L, double* factors) {
+  const long long f = blockIdx.x;
+  const Shape s = front_shape(L, f);
+  const int a = blockIdx.y * NB;
+  const int kb = min(a + NB, s.k) - a;
+  if (kb <= 0) return;
+  double* Pf = factors + f * L.fac_stride;
+  const double* M = L.aux + f * L.aux_stride + (long long)blockIdx.y * NB * NB;
+  for (int e = threadIdx.x; e < kb * NB; e += blockDim.x) {
+    const int i = e >> 6, j = e & 63;
+    if (j <= i) Pf[(long long)(a + i) * s.kp + a + j] = M[j * NB + i];
+  }
 }
 
 // C (+)= op((A diag(d)) B^T) with FP64 tensor-core MMA (mma.sync m8n8k4): 128x64
@@ -287,6 +474,14 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) bf[j] = bs[j * 8 * GLD + ks];
+      if (MODE == 2) {  // aux block: use its strict lower part, unit diagonal
+        const int tk = it * GBK + ks + (lane & 3);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int n = wx * 32 + j * 8 + (lane >> 2);
+          bf[j] = tk < n ? bf[j] : (tk == n ? 1.0 : 0.0);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
@@ -325,10 +520,17 @@ constexpr size_t kGemmSmem = sizeof(double) * (GSTAGES * (GBM + GBN) * GLD + GST
 static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
                                 unsigned long long* err, int a, int b, cudaStream_t st) {
   if (b - a <= NB) {
-    large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
-    const int rows = L.max_m - a;
-    dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GBM - 1) / GBM));
-    large_update_kernel<2><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, 0, 0, 0, a, 0);
+    const int rows = std::max(1, L.max_m - a - 1);
+    if (L.level_fronts <= kFusedBlockMaxFronts) {
+      // few fronts: one launch per block (redundant per-CTA diagonal factorization)
+      dim3 g((unsigned)L.n_fronts, (unsigned)((rows + TRB - 1) / TRB));
+      large_block_kernel<<<g, 256, kBlockSmem, st>>>(L, factors, a, thr, err);
+    } else {
+      // many fronts: register-tiled diagonal blocks, then the TRSM as a DMMA GEMM
+      large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
+      dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GBM - 1) / GBM));
+      large_update_kernel<2><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, 0, 0, 0, a, 0);
+    }
     return cudaGetLastError();
   }
   int mid = a + ((b - a) / 2 + NB - 1) / NB * NB;
@@ -357,6 +559,8 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                          (int)kGemmSmem);
     cudaFuncSetAttribute(large_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
+    cudaFuncSetAttribute(large_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBlockSmem);
     attr = true;
   }
   {
@@ -375,6 +579,12 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
            (unsigned)((L.max_upd + GBM - 1) / GBM));
     large_update_kernel<1><<<g, 256, kGemmSmem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
     e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (L.max_k > 0) {
+    dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
+    large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
+    e = cudaGetLastError();
   }
   return e;
 }
@@ -383,12 +593,12 @@ long long large_aux_doubles(int max_k) {
   return (long long)((max_k + NB - 1) / NB) * NB * NB;
 }
 
-int large_panel_launches(int max_k) {
+int large_panel_launches(int max_k, int n_fronts) {
   if (max_k <= 0) return 0;
-  if (max_k <= NB) return 2;
+  if (max_k <= NB) return n_fronts <= kFusedBlockMaxFronts ? 1 : 2;
   int mid = (max_k / 2 + NB - 1) / NB * NB;
   if (mid >= max_k) mid = NB;
-  return large_panel_launches(mid) + 1 + large_panel_launches(max_k - mid);
+  return large_panel_launches(mid, n_fronts) + 1 + large_panel_launches(max_k - mid, n_fronts);
 }
 
 }  // namespace tfb

@@ -90,6 +90,7 @@ class DeviceLevel:
         v.piv_off = self.piv_off.data_ptr()
         v.pat = self.pat.data_ptr()
         v.maps = self.maps.data_ptr()
+        v.level_fronts = lt.n_fronts
         self.aux_stride = int(lib.tf_level_aux_doubles(C.byref(v)))
         self.aux = None
         if self.aux_stride > 0:
