@@ -206,6 +206,14 @@ int32_t tf_level_launch_count(const tf_level_view* lv, int32_t nrhs, int32_t pha
  * kernels (a test and tuning knob).  Returns the previous value. */
 int32_t tf_set_small_max_m(int32_t m);
 
+/* Optional device timing of every kernel the library launches, by kernel class
+ * (CUDA events recorded on the launch stream around each launch).  collect()
+ * synchronises, returns the number of classes and fills per-class total ms and
+ * launch counts (arrays of n), then resets. */
+void tf_timing_enable(int32_t on);
+int32_t tf_timing_collect(double* ms, int64_t* count, int32_t n);
+const char* tf_timing_class_name(int32_t cls);
+
 /* Library build identification (arch, compile flags). */
 const char* tf_build_info(void);
 

@@ -64,7 +64,8 @@ EXPORTS = (
     "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
     "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
     "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_subtree_fusable",
-    "tf_subtree_factor", "tf_build_info",
+    "tf_subtree_factor", "tf_timing_enable", "tf_timing_collect", "tf_timing_class_name",
+    "tf_build_info",
 )
 
 _lib = None
@@ -124,6 +125,12 @@ def load() -> C.CDLL:
     lib.tf_subtree_fusable.restype = i32
     lib.tf_subtree_factor.argtypes = [vp, i32, vp, vp, vp, C.c_double, vp, vp]
     lib.tf_subtree_factor.restype = C.c_int
+    lib.tf_timing_enable.argtypes = [i32]
+    lib.tf_timing_enable.restype = None
+    lib.tf_timing_collect.argtypes = [vp, vp, i32]
+    lib.tf_timing_collect.restype = i32
+    lib.tf_timing_class_name.argtypes = [i32]
+    lib.tf_timing_class_name.restype = C.c_char_p
     lib.tf_build_info.argtypes = []
     lib.tf_build_info.restype = C.c_char_p
     _lib = lib
@@ -144,3 +151,13 @@ def i64p(arr):
 
 def i32p(arr):
     return arr.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def kernel_timing(lib, n: int = 32):
+    """Collect tf_timing: {class name: (total ms, launches)} (non-zero classes)."""
+    import numpy as np
+    ms = np.zeros(n)
+    cnt = np.zeros(n, dtype=np.int64)
+    k = lib.tf_timing_collect(ms.ctypes.data, cnt.ctypes.data, n)
+    return {lib.tf_timing_class_name(i).decode(): (float(ms[i]), int(cnt[i]))
+            for i in range(k) if cnt[i] > 0}

@@ -524,12 +524,18 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
     if (L.level_fronts <= kFusedBlockMaxFronts) {
       // few fronts: one launch per block (redundant per-CTA diagonal factorization)
       dim3 g((unsigned)L.n_fronts, (unsigned)((rows + TRB - 1) / TRB));
+      timer_begin(K_BLOCK, st);
       large_block_kernel<<<g, 256, kBlockSmem, st>>>(L, factors, a, thr, err);
+      timer_end(st);
     } else {
       // many fronts: register-tiled diagonal blocks, then the TRSM as a DMMA GEMM
+      timer_begin(K_DIAG, st);
       large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
+      timer_end(st);
       dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GBM - 1) / GBM));
+      timer_begin(K_TRSM, st);
       large_update_kernel<2><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, 0, 0, 0, a, 0);
+      timer_end(st);
     }
     return cudaGetLastError();
   }
@@ -539,7 +545,9 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
   if (e != cudaSuccess) return e;
   dim3 g((unsigned)L.n_fronts, (unsigned)((b - mid + GBN - 1) / GBN),
          (unsigned)((L.max_m - mid + GBM - 1) / GBM));
+  timer_begin(K_PANEL, st);
   large_update_kernel<0><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, mid, mid, b, a, mid);
+  timer_end(st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return panel_factor(L, factors, thr, err, mid, b, st);
@@ -566,7 +574,9 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   {
     const long long per = L.fac_stride + tri(L.max_upd, 0);
     const unsigned gx = (unsigned)std::min<long long>((per + 255) / 256, 1024);
+    timer_begin(K_ASSEMBLE, st);
     large_assemble_kernel<<<dim3(L.n_fronts, gx), 256, 0, st>>>(L, child_upd, factors, upd_out);
+    timer_end(st);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -577,13 +587,17 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   if (L.max_upd > 0 && L.max_k > 0) {
     dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + GBN - 1) / GBN),
            (unsigned)((L.max_upd + GBM - 1) / GBM));
+    timer_begin(K_SCHUR, st);
     large_update_kernel<1><<<g, 256, kGemmSmem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
+    timer_end(st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (L.max_k > 0) {
     dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
+    timer_begin(K_FINALIZE, st);
     large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
+    timer_end(st);
     e = cudaGetLastError();
   }
   return e;

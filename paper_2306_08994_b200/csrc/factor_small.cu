@@ -228,8 +228,10 @@ static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, c
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (L.n_fronts + GPC - 1) / GPC;
+  timer_begin(K_SMALL, st);
   kern<<<(unsigned)blocks, G * GPC, smem, st>>>(L, child_upd, elem, factors, upd_out, thr, err,
                                                 per);
+  timer_end(st);
   return cudaGetLastError();
 }
 
@@ -348,7 +350,9 @@ cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* 
   if (e != cudaSuccess) return e;
   const long long roots = lv[nlev - 1].n_fronts;
   const unsigned blocks = (unsigned)((roots + kSubNG - 1) / kSubNG);
+  timer_begin(K_SUBTREE, st);
   factor_subtree_kernel<<<blocks, kSubG * kSubNG, smem, st>>>(A, elem, upd_out, thr, err);
+  timer_end(st);
   return cudaGetLastError();
 }
 

@@ -395,14 +395,18 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
     auto kern = solve_fwd_small<G, GPC>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timer_begin(K_SOLVE_SMALL_FWD, st);
     kern<<<blocks, G * GPC, smem, st>>>(L, O, factors, w_in, in_rows, w_out, out_rows, y, nr, ldr,
                                         col0, per);
+    timer_end(st);
   } else {
     auto kern = solve_bwd_small<G, GPC>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    timer_begin(K_SOLVE_SMALL_BWD, st);
     kern<<<blocks, G * GPC, smem, st>>>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y,
                                         nr, ldr, col0, per);
+    timer_end(st);
   }
   return cudaGetLastError();
 }
@@ -455,14 +459,18 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
                                 st);
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
+  timer_begin(K_SOLVE_GATHER, st);
   solve_gather_fwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, C, w_child, child_rows, w_out, out_rows, y, nrhs);
+  timer_end(st);
   const size_t smem = sizeof(double) * (2 * SB * (size_t)nrhs + SB * SB);
   cudaFuncSetAttribute(solve_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int j0 = 0; j0 < L.max_k; j0 += SB) {
     const int rows = std::max(1, L.max_m - j0 - 1);
+    timer_begin(K_SOLVE_FWD_BLOCK, st);
     solve_fwd_block<<<dim3(nf, (unsigned)((rows + RB - 1) / RB)), 256, smem, st>>>(
         L, factors, w_out, out_rows, y, nrhs, j0);
+    timer_end(st);
   }
   return cudaGetLastError();
 }
@@ -477,8 +485,10 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
+  timer_begin(K_SOLVE_GATHER, st);
   solve_gather_bwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, PA, has_parent, x_parent, parent_rows, x_out, out_rows, y, nrhs);
+  timer_end(st);
   const int nchunk = (L.max_m + RB - 1) / RB;
   const size_t smp = sizeof(double) * RB * (size_t)nrhs;
   const size_t smb = sizeof(double) * (SB * (size_t)nrhs + SB * SB);
@@ -489,9 +499,13 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
     const int j0 = b * SB;
     const int rows = std::max(1, L.max_m - j0 - 1);
     const int used = (rows + RB - 1) / RB;
+    timer_begin(K_SOLVE_BWD_PARTIAL, st);
     solve_bwd_partial<<<dim3(nf, (unsigned)used), 256, smp, st>>>(L, factors, x_out, out_rows,
                                                                   nrhs, j0, work, nchunk);
+    timer_end(st);
+    timer_begin(K_SOLVE_BWD_BLOCK, st);
     solve_bwd_block<<<nf, 256, smb, st>>>(L, x_out, out_rows, y, nrhs, j0, work, nchunk);
+    timer_end(st);
   }
   return cudaGetLastError();
 }
@@ -507,7 +521,9 @@ cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, d
   long long total = n * nrhs;
   unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148 * 16);
   if (blocks == 0) return cudaSuccess;
+  timer_begin(K_PERMUTE, st);
   permute_rows_kernel<<<blocks, 256, 0, st>>>(idx, n, in, out, nrhs, scatter);
+  timer_end(st);
   return cudaGetLastError();
 }
 
