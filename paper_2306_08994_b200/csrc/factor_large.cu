@@ -13,6 +13,8 @@
 //   3. one DMMA update S -= L21 D L21^T over all k pivots.
 // Arithmetic replaced: engine.py:86-105 per pivot (Division, Multiplication,
 // Subtraction) and engine.py:537-545 (factorize_nested_loops inner loops).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace tfb {
@@ -344,23 +346,31 @@ __global__ void large_diag_finalize_kernel(LevelArgs L, double* factors) {
   }
 }
 
-// C (+)= op((A diag(d)) B^T) with FP64 tensor-core MMA (mma.sync m8n8k4): 128x64
-// CTA tiles, 8 warps of 32x32, 3-stage cp.async pipeline over K (BK = 16).
+// C (+)= op((A diag(d)) B^T) with FP64 tensor-core MMA (mma.sync m8n8k4): BMxBN
+// CTA tiles, 8 warps (4 x 2) of (BM/4)x(BN/2), ST-stage cp.async pipeline over K.
 // MODE 0 (panel): P[r][c] -= sum_t l_rt d_t l_ct, r in [row0, m), c in [col0, min(col1,k)),
 //                 r >= c, t in [t0, min(t1, k)).
 // MODE 1 (schur): S[i][j] -= sum_t l_{k+i,t} d_t l_{k+j,t}, i >= j, t in [0, k).
 // MODE 2 (trsm) : P[r][t0+c] = (sum_t P[r][t0+t] M[c][t]) / d_{t0+c}, r >= t0+kb,
 //                 c < kb (M = unit-lower inverse of the diagonal block at t0).
-constexpr int GBM = 128, GBN = 64, GBK = 16, GLD = GBK + 4, GSTAGES = 3;
+template <int BM_, int BN_, int BK_, int ST_, int WR_ = 4, int WC_ = 2>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, ST = ST_, LD = BK_ + 4;
+  static constexpr int WR = WR_, WC = WC_, NT = 32 * WR_ * WC_;  // warp grid, threads
+  static constexpr int WM = BM / WR, WN = BN / WC, MI = WM / 8, NJ = WN / 8;
+  static constexpr size_t smem = sizeof(double) * (ST * (BM + BN) * LD + ST * BK);
+};
 
-template <int MODE>
-__global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* factors,
+template <int MODE, class G>
+__global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double* factors,
                                                             double* upd, int row0, int col0,
                                                             int col1, int t0, int t1) {
+  constexpr int BM = G::BM, BN = G::BN, BK = G::BK, ST = G::ST, LD = G::LD;
+  constexpr int MI = G::MI, NJ = G::NJ;
   extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;                                  // [GSTAGES][GBM][GLD]
-  double* Bs = As + GSTAGES * GBM * GLD;             // [GSTAGES][GBN][GLD]
-  double* Ds = Bs + GSTAGES * GBN * GLD;             // [GSTAGES][GBK]
+  double* As = gsm;                       // [ST][BM][LD]
+  double* Bs = As + ST * BM * LD;         // [ST][BN][LD]
+  double* Ds = Bs + ST * BN * LD;         // [ST][BK]
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
@@ -370,35 +380,35 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
   int ldb = kp, aRow0, bRow0, nA, nB, aK0, bK0, kLen;
   long long tile_r0, tile_c0;
   if (MODE == 0) {
-    tile_r0 = row0 + (long long)blockIdx.z * GBM;
-    tile_c0 = col0 + (long long)blockIdx.y * GBN;
+    tile_r0 = row0 + (long long)blockIdx.z * BM;
+    tile_c0 = col0 + (long long)blockIdx.y * BN;
     const int cLim = min(col1, k);
-    if (tile_r0 >= m || tile_c0 >= cLim || tile_r0 + GBM <= tile_c0) return;
+    if (tile_r0 >= m || tile_c0 >= cLim || tile_r0 + BM <= tile_c0) return;
     aRow0 = (int)tile_r0;
     bRow0 = (int)tile_c0;
-    nA = min(GBM, m - aRow0);
-    nB = min(GBN, cLim - bRow0);
+    nA = min(BM, m - aRow0);
+    nB = min(BN, cLim - bRow0);
     aK0 = bK0 = t0;
     kLen = min(t1, k) - t0;
   } else if (MODE == 1) {
     const int u = m - k;
-    tile_r0 = (long long)blockIdx.z * GBM;
-    tile_c0 = (long long)blockIdx.y * GBN;
-    if (tile_r0 >= u || tile_c0 >= u || tile_r0 + GBM <= tile_c0) return;
+    tile_r0 = (long long)blockIdx.z * BM;
+    tile_c0 = (long long)blockIdx.y * BN;
+    if (tile_r0 >= u || tile_c0 >= u || tile_r0 + BM <= tile_c0) return;
     aRow0 = k + (int)tile_r0;
     bRow0 = k + (int)tile_c0;
-    nA = min(GBM, u - (int)tile_r0);
-    nB = min(GBN, u - (int)tile_c0);
+    nA = min(BM, u - (int)tile_r0);
+    nB = min(BN, u - (int)tile_c0);
     aK0 = bK0 = 0;
     kLen = k;
   } else {
     const int kb = min(t0 + NB, k) - t0;
     if (kb <= 0) return;
-    tile_r0 = t0 + kb + (long long)blockIdx.z * GBM;
+    tile_r0 = t0 + kb + (long long)blockIdx.z * BM;
     tile_c0 = t0;
     if (tile_r0 >= m) return;
     aRow0 = (int)tile_r0;
-    nA = min(GBM, m - aRow0);
+    nA = min(BM, m - aRow0);
     Bbase = L.aux + f * L.aux_stride + (long long)(t0 / NB) * NB * NB;
     ldb = NB;
     bRow0 = 0;
@@ -409,98 +419,101 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
   }
   if (kLen <= 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wy = warp >> 1, wx = warp & 1;  // 4 x 2 warps of 32x32
-  const int nk = (kLen + GBK - 1) / GBK;
+  const int wy = warp / G::WC, wx = warp % G::WC;  // WR x WC warps
+  const int nk = (kLen + BK - 1) / BK;
+  constexpr int CPR = BK / 2;  // 16-byte chunks per tile row
 
   auto issue = [&](int it) {
-    const int stage = it % GSTAGES;
-    const int kt = it * GBK;
-    double* as = As + stage * GBM * GLD;
-    double* bs = Bs + stage * GBN * GLD;
+    const int stage = it % ST;
+    const int kt = it * BK;
+    double* as = As + stage * BM * LD;
+    double* bs = Bs + stage * BN * LD;
 #pragma unroll
-    for (int q = 0; q < 4; q++) {  // A: 128 rows x 8 chunks of 2 doubles
-      const int ch = tid + q * 256;
-      const int r = ch >> 3, cc = (ch & 7) * 2;
+    for (int q = 0; q < (BM * CPR + G::NT - 1) / G::NT; q++) {
+      const int ch = tid + q * G::NT;
+      if (ch >= BM * CPR) break;
+      const int r = ch / CPR, cc = (ch % CPR) * 2;
       const int t = kt + cc;
       const bool v = r < nA && t < kLen;
       const double* src = v ? Pf + (long long)(aRow0 + r) * kp + aK0 + t : Pf;
-      cp_async16(as + r * GLD + cc, src, v);
+      cp_async16(as + r * LD + cc, src, v);
     }
 #pragma unroll
-    for (int q = 0; q < 2; q++) {  // B: 64 rows x 8 chunks
-      const int ch = tid + q * 256;
-      const int r = ch >> 3, cc = (ch & 7) * 2;
+    for (int q = 0; q < (BN * CPR + G::NT - 1) / G::NT; q++) {
+      const int ch = tid + q * G::NT;
+      if (ch >= BN * CPR) break;
+      const int r = ch / CPR, cc = (ch % CPR) * 2;
       const int t = kt + cc;
       const bool v = r < nB && t < kLen;
       const double* src = v ? Bbase + (long long)(bRow0 + r) * ldb + bK0 + t : Bbase;
-      cp_async16(bs + r * GLD + cc, src, v);
+      cp_async16(bs + r * LD + cc, src, v);
     }
-    if (MODE != 2 && tid < GBK / 2) {
+    if (MODE != 2 && tid < CPR) {
       const int t = kt + tid * 2;
-      cp_async16(Ds + stage * GBK + tid * 2, t < kLen ? dvec + aK0 + t : dvec, t < kLen);
+      cp_async16(Ds + stage * BK + tid * 2, t < kLen ? dvec + aK0 + t : dvec, t < kLen);
     }
   };
 
-  double acc[4][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < MI; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int it = 0; it < GSTAGES - 1; it++) {
+  for (int it = 0; it < ST - 1; it++) {
     if (it < nk) issue(it);
     cp_async_commit();
   }
   for (int it = 0; it < nk; it++) {
-    cp_async_wait<GSTAGES - 2>();
+    cp_async_wait<ST - 2>();
     __syncthreads();
-    if (it + GSTAGES - 1 < nk) issue(it + GSTAGES - 1);
+    if (it + ST - 1 < nk) issue(it + ST - 1);
     cp_async_commit();
-    const int stage = it % GSTAGES;
-    const double* as = As + stage * GBM * GLD + (wy * 32 + (lane >> 2)) * GLD + (lane & 3);
-    const double* bs = Bs + stage * GBN * GLD + (wx * 32 + (lane >> 2)) * GLD + (lane & 3);
-    const double* ds = Ds + stage * GBK + (lane & 3);
+    const int stage = it % ST;
+    const double* as = As + stage * BM * LD + (wy * G::WM + (lane >> 2)) * LD + (lane & 3);
+    const double* bs = Bs + stage * BN * LD + (wx * G::WN + (lane >> 2)) * LD + (lane & 3);
+    const double* ds = Ds + stage * BK + (lane & 3);
 #pragma unroll
-    for (int ks = 0; ks < GBK; ks += 4) {
-      double af[4], bf[4];
+    for (int ks = 0; ks < BK; ks += 4) {
+      double af[MI], bf[NJ];
       if (MODE == 2) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) af[i] = as[i * 8 * GLD + ks];
+        for (int i = 0; i < MI; i++) af[i] = as[i * 8 * LD + ks];
       } else {
         const double dk = ds[ks];
 #pragma unroll
-        for (int i = 0; i < 4; i++) af[i] = as[i * 8 * GLD + ks] * dk;
+        for (int i = 0; i < MI; i++) af[i] = as[i * 8 * LD + ks] * dk;
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) bf[j] = bs[j * 8 * GLD + ks];
+      for (int j = 0; j < NJ; j++) bf[j] = bs[j * 8 * LD + ks];
       if (MODE == 2) {  // aux block: use its strict lower part, unit diagonal
-        const int tk = it * GBK + ks + (lane & 3);
+        const int tk = it * BK + ks + (lane & 3);
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int n = wx * 32 + j * 8 + (lane >> 2);
+        for (int j = 0; j < NJ; j++) {
+          const int n = wx * G::WN + j * 8 + (lane >> 2);
           bf[j] = tk < n ? bf[j] : (tk == n ? 1.0 : 0.0);
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; i++)
+      for (int i = 0; i < MI; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma884(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < NJ; j++) dmma884(acc[i][j], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
   if (MODE == 2) __syncthreads();  // every A tile row is read before it is overwritten
   double* out = MODE == 1 ? upd + f * L.upd_stride : Pf;
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const int rl = wy * 32 + i * 8 + (lane >> 2);
+  for (int i = 0; i < MI; i++) {
+    const int rl = wy * G::WM + i * 8 + (lane >> 2);
     if (rl >= nA) continue;
     const long long R = tile_r0 + rl;
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
+    for (int j = 0; j < NJ; j++) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const int cl = wx * 32 + j * 8 + 2 * (lane & 3) + h;
+        const int cl = wx * G::WN + j * 8 + 2 * (lane & 3) + h;
         if (cl >= nB) continue;
         const long long C = tile_c0 + cl;
         if (MODE == 2) {
@@ -515,7 +528,42 @@ __global__ void __launch_bounds__(256) large_update_kernel(LevelArgs L, double* 
   }
 }
 
-constexpr size_t kGemmSmem = sizeof(double) * (GSTAGES * (GBM + GBN) * GLD + GSTAGES * GBK);
+// Tile shapes measured on B200 (tools/schur_sweep.sh): 64x64 tiles of 8 warps
+// with a 2-stage pipeline keep the most warps resident and win on every level.
+using GTrsm = GemmCfg<64, 64, 16, 2>;   // N = 64 = one diagonal block
+using GPanel = GemmCfg<64, 64, 16, 2>;
+using GSchurA = GemmCfg<64, 64, 16, 2>;        // 8 warps of 16x32
+using GSchurB = GemmCfg<64, 64, 8, 4>;
+using GSchurC = GemmCfg<64, 64, 16, 3, 2, 2>;  // 4 warps of 32x32
+using GSchurD = GemmCfg<64, 32, 16, 3, 4, 1>;  // 4 warps of 16x32
+using GSchurE = GemmCfg<128, 64, 16, 3>;
+
+template <int MODE, class G>
+static void gemm_attr() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(large_update_kernel<MODE, G>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem);
+    done = true;
+  }
+}
+
+template <class G>
+static void launch_schur(const LevelArgs& L, double* factors, double* upd_out, cudaStream_t st) {
+  gemm_attr<1, G>();
+  dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + G::BN - 1) / G::BN),
+         (unsigned)((L.max_upd + G::BM - 1) / G::BM));
+  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
+}
+
+static int gemm_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_SCHUR_CFG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
 static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
                                 unsigned long long* err, int a, int b, cudaStream_t st) {
@@ -532,9 +580,11 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
       timer_begin(K_DIAG, st);
       large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
       timer_end(st);
-      dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GBM - 1) / GBM));
+      dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GTrsm::BM - 1) / GTrsm::BM));
+      gemm_attr<2, GTrsm>();
       timer_begin(K_TRSM, st);
-      large_update_kernel<2><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, 0, 0, 0, a, 0);
+      large_update_kernel<2, GTrsm><<<g, GTrsm::NT, GTrsm::smem, st>>>(L, factors, nullptr, 0, 0, 0,
+                                                                   a, 0);
       timer_end(st);
     }
     return cudaGetLastError();
@@ -543,10 +593,12 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
   if (mid >= b) mid = a + NB;
   cudaError_t e = panel_factor(L, factors, thr, err, a, mid, st);
   if (e != cudaSuccess) return e;
-  dim3 g((unsigned)L.n_fronts, (unsigned)((b - mid + GBN - 1) / GBN),
-         (unsigned)((L.max_m - mid + GBM - 1) / GBM));
+  dim3 g((unsigned)L.n_fronts, (unsigned)((b - mid + GPanel::BN - 1) / GPanel::BN),
+         (unsigned)((L.max_m - mid + GPanel::BM - 1) / GPanel::BM));
+  gemm_attr<0, GPanel>();
   timer_begin(K_PANEL, st);
-  large_update_kernel<0><<<g, 256, kGemmSmem, st>>>(L, factors, nullptr, mid, mid, b, a, mid);
+  large_update_kernel<0, GPanel><<<g, GPanel::NT, GPanel::smem, st>>>(L, factors, nullptr, mid, mid, b,
+                                                                  a, mid);
   timer_end(st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -561,12 +613,6 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(large_update_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kGemmSmem);
-    cudaFuncSetAttribute(large_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kGemmSmem);
-    cudaFuncSetAttribute(large_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kGemmSmem);
     cudaFuncSetAttribute(large_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBlockSmem);
     attr = true;
@@ -585,10 +631,14 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
     if (e != cudaSuccess) return e;
   }
   if (L.max_upd > 0 && L.max_k > 0) {
-    dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + GBN - 1) / GBN),
-           (unsigned)((L.max_upd + GBM - 1) / GBM));
     timer_begin(K_SCHUR, st);
-    large_update_kernel<1><<<g, 256, kGemmSmem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
+    switch (gemm_variant()) {
+      case 1: launch_schur<GSchurB>(L, factors, upd_out, st); break;
+      case 2: launch_schur<GSchurC>(L, factors, upd_out, st); break;
+      case 3: launch_schur<GSchurD>(L, factors, upd_out, st); break;
+      case 4: launch_schur<GSchurE>(L, factors, upd_out, st); break;
+      default: launch_schur<GSchurA>(L, factors, upd_out, st); break;
+    }
     timer_end(st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
