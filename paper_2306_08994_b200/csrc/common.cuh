@@ -103,6 +103,15 @@ __host__ __device__ __forceinline__ long long tri(long long r, long long c) {
   return r * (r + 1) / 2 + c;
 }
 
+// 32-bit variants for shared-memory fronts (all indices < 2^31).
+__host__ __device__ __forceinline__ int tri32(int r, int c) { return ((r * (r + 1)) >> 1) + c; }
+__device__ __forceinline__ int tri_row32(int e) {  // exact for e < 2^22
+  int r = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  r -= (((r * (r + 1)) >> 1) > e);
+  r += ((((r + 1) * (r + 2)) >> 1) <= e);
+  return r;
+}
+
 // Row of packed index e (exact for any e < 2^50).
 __device__ __forceinline__ int tri_row(long long e) {
   int r;

@@ -44,7 +44,7 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
                                              double* __restrict__ upd_dst, double threshold,
                                              unsigned long long* err, int t, int bar) {
   const int m = S.m, k = S.k, kp = S.kp, u = m - k;
-  const int nF = (int)tri(m, 0);
+  const int nF = (int)tri32(m, 0);
 
   for (int e = t; e < nF; e += G) F[e] = 0.0;
   for (int i = t; i < S.len0; i += G) mp[i] = L.maps[S.off0 + i];
@@ -55,16 +55,16 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
   for (int c = 0; c < S.nsrc; c++) {
     const int len = c == 0 ? S.len0 : S.len1;
     const int* cm = mp + (c == 0 ? 0 : S.len0);
-    const int n = (int)tri(len, 0);
+    const int n = (int)tri32(len, 0);
     int beg, end;
     chunk_of(n, G, t, beg, end);
     if (beg < end) {
-      int a = tri_row(beg), b = beg - (int)tri(a, 0);
+      int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
       if (L.is_leaf) {
         const double* E = src0;
         for (int e = beg; e < end; e++) {
           const int R = cm[a], C = cm[b];
-          F[R > C ? tri(R, C) : tri(C, R)] += E[a * L.elem_ld + b];
+          F[R > C ? tri32(R, C) : tri32(C, R)] += E[a * L.elem_ld + b];
           if (++b > a) { a++; b = 0; }
         }
       } else {
@@ -78,13 +78,13 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
 #pragma unroll
           for (int q = 0; q < U; q++) {
             const int R = cm[a], C = cm[b];
-            F[R > C ? tri(R, C) : tri(C, R)] += v[q];
+            F[R > C ? tri32(R, C) : tri32(C, R)] += v[q];
             if (++b > a) { a++; b = 0; }
           }
         }
         for (; e < end; e++) {
           const int R = cm[a], C = cm[b];
-          F[R > C ? tri(R, C) : tri(C, R)] += src[e];
+          F[R > C ? tri32(R, C) : tri32(C, R)] += src[e];
           if (++b > a) { a++; b = 0; }
         }
       }
@@ -95,12 +95,12 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
   // (2) panel: right-looking over the k pivot columns, updates confined to them
   const long long piv0 = L.piv_off[f];
   for (int c = 0; c < k; c++) {
-    const double d = F[tri(c, c)];
+    const double d = F[tri32(c, c)];
     if (t == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-    for (int r = c + 1 + t; r < m; r += G) lv[r] = F[tri(r, c)] / d;
+    for (int r = c + 1 + t; r < m; r += G) lv[r] = F[tri32(r, c)] / d;
     group_sync<G>(bar);
     for (int r = c + 1 + t; r < m; r += G) {
-      double* row = F + tri(r, 0);
+      double* row = F + tri32(r, 0);
       const double frc = row[c];
       const int smax = min(r, k - 1);
       for (int s = c + 1; s <= smax; s++) row[s] -= lv[s] * frc;
@@ -111,7 +111,7 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
 
   // (3) Schur block: F[k+i][k+j] -= sum_t l(k+i,t) d_t l(k+j,t), i >= j
   if (k > 0 && u > 0) {
-    for (int c = t; c < k; c += G) lv[c] = F[tri(c, c)];  // pivots
+    for (int c = t; c < k; c += G) lv[c] = F[tri32(c, c)];  // pivots
     group_sync<G>(bar);
     if constexpr (G >= 32) {
       const int warp = t >> 5, lane = t & 31, g8 = lane >> 2, tq = lane & 3;
@@ -122,8 +122,8 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
         while ((I + 1) * (I + 2) / 2 <= tile) I++;
         const int J = tile - I * (I + 1) / 2;
         const int ra = k + 8 * I + g8, rb = k + 8 * J + g8;
-        const double* arow = F + tri(min(ra, m - 1), 0);
-        const double* brow = F + tri(min(rb, m - 1), 0);
+        const double* arow = F + tri32(min(ra, m - 1), 0);
+        const double* brow = F + tri32(min(rb, m - 1), 0);
         const bool va = ra < m, vb = rb < m;
         double acc[2] = {0.0, 0.0};
         for (int kk = 0; kk < k; kk += 4) {
@@ -136,20 +136,20 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int Cc = k + 8 * J + 2 * tq + h;
-          if (R < m && Cc <= R) F[tri(R, Cc)] -= acc[h];
+          if (R < m && Cc <= R) F[tri32(R, Cc)] -= acc[h];
         }
       }
     } else {
       int beg, end;
-      chunk_of((int)tri(u, 0), G, t, beg, end);
+      chunk_of((int)tri32(u, 0), G, t, beg, end);
       if (beg < end) {
-        int a = tri_row(beg), b = beg - (int)tri(a, 0);
+        int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
         for (int e = beg; e < end; e++) {
-          const double* ra = F + tri(k + a, 0);
-          const double* rb = F + tri(k + b, 0);
+          const double* ra = F + tri32(k + a, 0);
+          const double* rb = F + tri32(k + b, 0);
           double acc = 0.0;
           for (int q = 0; q < k; q++) acc += ra[q] * lv[q] * rb[q];
-          F[tri(k + a, k + b)] -= acc;
+          F[tri32(k + a, k + b)] -= acc;
           if (++b > a) { a++; b = 0; }
         }
       }
@@ -164,20 +164,20 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
     if (beg < end) {
       int r = beg / k, c = beg - r * k;
       for (int e = beg; e < end; e++) {
-        if (c <= r) fac_out[(long long)r * kp + c] = F[tri(r, c)];
+        if (c <= r) fac_out[(long long)r * kp + c] = F[tri32(r, c)];
         if (++c == k) { c = 0; r++; }
       }
     }
     double* dv = fac_out + (long long)m * kp;
-    for (int c = t; c < kp; c += G) dv[c] = c < k ? F[tri(c, c)] : 0.0;
+    for (int c = t; c < kp; c += G) dv[c] = c < k ? F[tri32(c, c)] : 0.0;
   }
   if (u > 0) {
     int beg, end;
-    chunk_of((int)tri(u, 0), G, t, beg, end);
+    chunk_of((int)tri32(u, 0), G, t, beg, end);
     if (beg < end) {
-      int a = tri_row(beg), b = beg - (int)tri(a, 0);
+      int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
       for (int e = beg; e < end; e++) {
-        upd_dst[e] = F[tri(k + a, k + b)];
+        upd_dst[e] = F[tri32(k + a, k + b)];
         if (++b > a) { a++; b = 0; }
       }
     }
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(G* GPC)
   if (f >= L.n_fronts) return;  // whole group exits; syncs are group-local
   unsigned char* my = smem_raw + (size_t)gid * smem_per_group;
   double* F = reinterpret_cast<double*>(my);
-  double* lv = F + tri(L.max_m, 0);
+  double* lv = F + tri32(L.max_m, 0);
   int* mp = reinterpret_cast<int*>(lv + L.max_m);
   const Shape S = front_shape(L, f);
   const double* s0 = L.is_leaf ? elem + f * L.elem_stride
@@ -238,13 +238,14 @@ static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, c
 cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, const double* elem,
                                 double* factors, double* upd_out, double thr,
                                 unsigned long long* err, cudaStream_t st) {
+  // groups sized so that a CTA's shared memory stays small enough for several
+  // CTAs per SM (occupancy hides the shared-memory latency of the pivot loop)
   const int mm = L.max_m;
   if (mm <= 8) return launch_small_t<4, 64>(L, child_upd, elem, factors, upd_out, thr, err, st);
   if (mm <= 16) return launch_small_t<8, 32>(L, child_upd, elem, factors, upd_out, thr, err, st);
   if (mm <= 24) return launch_small_t<16, 16>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 48) return launch_small_t<32, 8>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 80) return launch_small_t<64, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 128) return launch_small_t<128, 2>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 48) return launch_small_t<32, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  if (mm <= 80) return launch_small_t<128, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
   return launch_small_t<256, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
 }
 
@@ -280,12 +281,12 @@ __global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
   for (int L = 0; L < A.nlev; L++) {
     const LevelArgs& lv = A.lv[L];
     double* F = reinterpret_cast<double*>(ws);
-    double* lvec = F + tri(lv.max_m, 0);
+    double* lvec = F + tri32(lv.max_m, 0);
     int* mp = reinterpret_cast<int*>(lvec + lv.max_m);
     double* prev = arena[(L + 1) & 1];
     double* cur = arena[L & 1];
-    const int cst = L > 0 ? (int)tri(A.lv[L - 1].max_upd, 0) : 0;
-    const int ost = (int)tri(lv.max_upd, 0);
+    const int cst = L > 0 ? (int)tri32(A.lv[L - 1].max_upd, 0) : 0;
+    const int ost = (int)tri32(lv.max_upd, 0);
     const long long base = root << (top - L);
     const long long cnt = min((long long)1 << (top - L), (long long)lv.n_fronts - base);
     for (long long i = 0; i < cnt; i++) {
@@ -309,7 +310,7 @@ static size_t subtree_group_bytes(const LevelArgs* lv, int nlev, int arena[2], i
     mm = std::max(mm, lv[L].max_m);
     if (L < nlev - 1) {
       const int nf = 1 << (nlev - 1 - L);
-      arena[L & 1] = std::max(arena[L & 1], nf * (int)tri(lv[L].max_upd, 0));
+      arena[L & 1] = std::max(arena[L & 1], nf * (int)tri32(lv[L].max_upd, 0));
     }
   }
   arena[0] = (arena[0] + 1) & ~1;
