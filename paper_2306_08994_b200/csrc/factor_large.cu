@@ -21,12 +21,36 @@ namespace tfb {
 
 constexpr int NB = 64;  // diagonal block width
 
-__global__ void large_assemble_kernel(LevelArgs L, const double* __restrict__ child_upd,
-                                      double* __restrict__ factors, double* __restrict__ upd) {
-  const long long f = blockIdx.x;  // fronts on x (no 65535 limit), chunks on y
+// Optional per-phase clock stamps of CTA 0 (tools/diag_bench.cu builds with it).
+#ifdef TFB_PHASE_CLOCK
+__device__ long long g_phase_clk[32];
+#define TFB_PHASE(i)                                                          \
+  do {                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_phase_clk[i] = clock64(); \
+  } while (0)
+#else
+#define TFB_PHASE(i) \
+  do {               \
+  } while (0)
+#endif
+
+// Warp per front row (rows dealt round-robin over the CTAs of the front), lanes
+// across the row's columns: the panel row P[r][0, kp) and, for r >= k, the
+// packed Schur row S[r-k][0, r-k].  The row's child indices are warp-uniform;
+// all index math is 32-bit (a front's packed child block is < 2^31 entries).
+constexpr int kAsmWarps = 8, kAsmRowsPerWarp = 4;
+__device__ __forceinline__ double child_entry(const double* __restrict__ src, int i, int tri_i,
+                                              int j) {
+  // packed lower-triangular (i, j) of the child block; -1 = not in this child
+  if (i < 0 || j < 0) return 0.0;
+  return src[i >= j ? tri_i + j : tri32(j, i)];
+}
+__global__ void __launch_bounds__(32 * kAsmWarps)
+    large_assemble_kernel(LevelArgs L, const double* __restrict__ child_upd,
+                          double* __restrict__ factors, double* __restrict__ upd) {
+  const long long f = blockIdx.x;  // fronts on x (no 65535 limit), row groups on y
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  const long long nPk = (long long)m * kp, nP = nPk + kp, nS = tri(m - k, 0);
   double* Pf = factors + f * L.fac_stride;
   double* Sf = upd + f * L.upd_stride;
   const int* inv0 = L.maps + s.ioff;
@@ -34,151 +58,393 @@ __global__ void large_assemble_kernel(LevelArgs L, const double* __restrict__ ch
   const double* src0 = child_upd + L.child_slot(f, 0) * L.child_upd_stride;
   const double* src1 = child_upd + L.child_slot(f, 1) * L.child_upd_stride;
   const bool two = s.nsrc == 2;
-  for (long long e = blockIdx.y * (long long)blockDim.x + threadIdx.x; e < nP + nS;
-       e += (long long)gridDim.y * blockDim.x) {
-    int r, c;
-    double* dst;
-    if (e < nPk) {
-      r = (int)(e / kp);
-      c = (int)(e - (long long)r * kp);
-      dst = Pf + e;
-      if (c >= k || c > r) { *dst = 0.0; continue; }
-    } else if (e < nP) {
-      Pf[e] = 0.0;
-      continue;
-    } else {
-      const long long e2 = e - nP;
-      const int a = tri_row(e2);
-      r = k + a;
-      c = k + (int)(e2 - tri(a, 0));
-      dst = Sf + e2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.y == 0 && warp == 0)
+    for (int c = lane; c < kp; c += 32) Pf[(long long)m * kp + c] = 0.0;  // d (set by the diag)
+  for (int r = blockIdx.y * kAsmWarps + warp; r < m; r += gridDim.y * kAsmWarps) {
+    const int i0 = inv0[r], t0 = i0 >= 0 ? tri32(i0, 0) : 0;
+    const int i1 = two ? inv1[r] : -1, t1 = i1 >= 0 ? tri32(i1, 0) : 0;
+    double* prow = Pf + (long long)r * kp;
+    const int pc = min(r + 1, k);
+    for (int c = lane; c < kp; c += 32) {
+      double v = 0.0;
+      if (c < pc) {
+        v = child_entry(src0, i0, t0, inv0[c]);
+        if (two) v += child_entry(src1, i1, t1, inv1[c]);
+      }
+      prow[c] = v;
     }
-    double v = 0.0;
-    {
-      const int i = inv0[r], j = inv0[c];
-      if (i >= 0 && j >= 0) v += src0[i > j ? tri(i, j) : tri(j, i)];
+    if (r >= k) {
+      const int a = r - k;
+      double* srow = Sf + tri32(a, 0);
+      for (int c = lane; c <= a; c += 32) {
+        double v = child_entry(src0, i0, t0, inv0[k + c]);
+        if (two) v += child_entry(src1, i1, t1, inv1[k + c]);
+        srow[c] = v;
+      }
     }
-    if (two) {
-      const int i = inv1[r], j = inv1[c];
-      if (i >= 0 && j >= 0) v += src1[i > j ? tri(i, j) : tri(j, i)];
-    }
-    *dst = v;
   }
 }
 
-// Factor the diagonal block [a, a+kb) of every front's panel (LDL^T, in shared
-// memory), store l (scaled) and d, and the unit-lower inverse M = L_bb^-1 in aux.
-// 256 threads: thread t owns row r = t/4, columns [16h, 16h+16) with h = t%4, held
-// in registers.  One barrier per pivot: the owners of column c publish it to a
-// double-buffered shared vector, every thread applies the rank-1 update to its
-// registers.  The inverse is formed the same way, one published row per step.
-__global__ void __launch_bounds__(256) large_diag_kernel(LevelArgs L, double* factors, int a,
-                                                          double threshold,
-                                                          unsigned long long* err) {
-  constexpr int Q = 4, W = NB / Q;  // four threads per row, W columns each
-  __shared__ double buf[2][NB];
+// ---------------------------------------------------------------- diagonal blocks
+// Warp-level LDL^T of a 32x32 symmetric block held in registers: lane r owns
+// row r (v[j] = a(r, j) for j <= r, v[j > r] = 0; padding rows are unit rows).
+// Pivot c: d = a(c, c) from lane c, l(r, c) = a(r, c) / d, and the rank-1 update
+// a(r, j) -= l(r, c) a(j, c) takes a(j, c) from lane j by shuffle.  On return
+// v[j < r] = l(r, j) and v[r] = d_r.  No shared memory, no barriers.
+__device__ __forceinline__ void warp_ldl32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int c = 0; c < 32; c++) {
+    const double d = __shfl_sync(0xffffffffu, v[c], c);
+    const double l = v[c] * (1.0 / d);
+#pragma unroll
+    for (int j = c + 1; j < 32; j++) {
+      const double ajc = __shfl_sync(0xffffffffu, v[c], j);
+      if (lane >= j) v[j] -= l * ajc;
+    }
+    if (lane > c) v[c] = l;
+  }
+}
+
+// Row `lane` of M = L^-1 for the unit-lower L in v (warp_ldl32 output):
+// w[j] = M(lane, j), j < lane; w[lane] = 1; w[j > lane] = 0.  Right-looking:
+// after step t row t is final and rows below subtract l(r, t) M(t, :).
+__device__ __forceinline__ void warp_inv32(const double (&v)[32], double (&w)[32], int lane) {
+#pragma unroll
+  for (int j = 0; j < 32; j++) w[j] = j == lane ? 1.0 : 0.0;
+#pragma unroll
+  for (int t = 0; t < 31; t++) {
+#pragma unroll
+    for (int j = 0; j <= t; j++) {
+      const double mtj = __shfl_sync(0xffffffffu, w[j], t);
+      if (lane > t) w[j] -= v[t] * mtj;
+    }
+  }
+}
+
+__device__ __forceinline__ double reg_pick(const double (&v)[32], int i) {
+  double x = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; j++) x = j == i ? v[j] : x;
+  return x;
+}
+
+// One warp per front: diagonal blocks of width kb <= 32 (4 fronts per CTA).
+// Writes l (strict lower) and d into the panel, d into the pivot vector and
+// the aux block (strict lower = M, diagonal = d, strict upper = l^T).
+__global__ void __launch_bounds__(128) large_diag32_kernel(LevelArgs L, double* factors, int a,
+                                                            double threshold,
+                                                            unsigned long long* err) {
+  const int lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (f >= L.n_fronts) return;
+  const Shape s = front_shape(L, f);
+  const int kb = min(a + NB, s.k) - a;
+  if (kb <= 0) return;
+  double* Pf = factors + f * L.fac_stride;
+  double v[32];
+  const double* prow = Pf + (long long)(a + lane) * s.kp + a;
+#pragma unroll
+  for (int j = 0; j < 32; j++)
+    v[j] = lane < kb ? (j <= lane ? prow[j] : 0.0) : (j == lane ? 1.0 : 0.0);
+  warp_ldl32(v, lane);
+  const double dr = reg_pick(v, lane);
+  if (lane < kb && fabs(dr) <= threshold)
+    record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + a + lane));
+  double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
+  if (lane < kb) {
+    double* pw = Pf + (long long)(a + lane) * s.kp + a;
+#pragma unroll
+    for (int j = 0; j < 32; j++)
+      if (j <= lane) pw[j] = v[j];
+    Pf[(long long)s.m * s.kp + a + lane] = dr;
+  }
+  double w[32];
+  warp_inv32(v, w, lane);
+  // aux rows/cols [0, 32) of the 64x64 block; the rest is the identity
+#pragma unroll
+  for (int j = 0; j < 32; j++) {
+    if (j < lane) {
+      M[lane * NB + j] = w[j];
+      M[j * NB + lane] = lane < kb ? v[j] : 0.0;
+    }
+  }
+  M[lane * NB + lane] = lane < kb ? dr : 1.0;
+  for (int e = lane; e < 32 * NB; e += 32) {  // rows 32..63: identity
+    const int i = 32 + e / NB, j = e % NB;
+    M[i * NB + j] = i == j ? 1.0 : 0.0;
+  }
+  for (int e = lane; e < 32 * 32; e += 32) M[(e >> 5) * NB + 32 + (e & 31)] = 0.0;
+}
+
+// 64x64 diagonal-block LDL^T + inverse in shared memory, few barriers:
+//   for each 16-column panel: one warp factors it warp-synchronously (lane
+//   owns rows c0+lane and c0+32+lane in registers, pivot columns broadcast by
+//   shuffles, fully unrolled so register indices are static), then all warps
+//   apply the rank-16 update to the trailing block with DMMA;
+//   M = L^-1 from 16x16 diagonal-block inverses (one warp each) and block
+//   rows M_ij = -M_ii sum_{t=j}^{i-1} L_it M_tj.
+// D (ld DLD): the block with unit rows beyond kb; on return its lower part
+// holds l (strict) and d (diagonal), dv = d, Mi = L^-1 (unit diagonal, zero
+// upper part).  NT threads; ends with a barrier.
+constexpr int DLD = NB + 1;
+
+// 1/d: hardware approximation refined by two Newton steps (full double
+// precision for normal d; shorter dependency chain than the IEEE division).
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+
+__device__ __forceinline__ void panel16_warp(double (*D)[DLD], double* dv, int c0, int lane) {
+  const int r0 = c0 + lane, r1 = c0 + 32 + lane;
+  const bool h0 = r0 < NB, h1 = r1 < NB;
+  double x0[16], x1[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    x0[j] = h0 ? D[r0][c0 + j] : 0.0;
+    x1[j] = h1 ? D[r1][c0 + j] : 0.0;
+  }
+#pragma unroll
+  for (int cc = 0; cc < 16; cc++) {
+    const double d = __shfl_sync(0xffffffffu, x0[cc], cc);
+    const double inv = rcp_nr(d);
+    const double l0 = x0[cc] * inv, l1 = x1[cc] * inv;
+#pragma unroll
+    for (int jj = cc + 1; jj < 16; jj++) {
+      const double ajc = __shfl_sync(0xffffffffu, x0[cc], jj);  // a(c0+jj, c0+cc)
+      x0[jj] -= l0 * ajc;  // (entries right of the diagonal are never read)
+      x1[jj] -= l1 * ajc;
+    }
+    if (lane > cc) x0[cc] = l0;
+    x1[cc] = l1;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    if (h0 && j <= lane) D[r0][c0 + j] = x0[j];
+    if (h1) D[r1][c0 + j] = x1[j];
+  }
+  if (lane < 16) {
+    double x = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) x = j == lane ? x0[j] : x;
+    dv[c0 + lane] = x;
+  }
+}
+
+// Row r of the inverse of the 16x16 unit-lower block of D at (o, o), by the
+// half-warp owning it (lane & 15 = r; width-16 shuffles).  Writes the full
+// 16x16 block of Mi (unit diagonal, zeros above).
+__device__ __forceinline__ void inv16_half(double (*D)[DLD], double (*Mi)[DLD], int o, int r) {
+  double l[16], w[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    l[j] = j < r ? D[o + r][o + j] : 0.0;
+    w[j] = j == r ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int t = 0; t < 15; t++) {
+#pragma unroll
+    for (int j = 0; j <= t; j++) {
+      const double mtj = __shfl_sync(0xffffffffu, w[j], t, 16);
+      if (r > t) w[j] -= l[t] * mtj;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++) Mi[o + r][o + j] = w[j];
+}
+
+// C = alpha A B for shared-memory operands on 8x8 DMMA tiles (A(i,k) =
+// A[i*lda+k], B(k,n) = B[k*ldb+n]; M, N multiples of 8, K of 4).
+template <int NT, int MT>
+__device__ __forceinline__ void smem_gemm(double* C, int ldc, const double* A, int lda,
+                                          const double* B, int ldb, int M, int N, int K,
+                                          double alpha) {
+  // MT = tiles per warp (ceil(tiles / warps)), accumulated side by side
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, tq = lane & 3;
+  const int TN = N >> 3, ntile = (M >> 3) * TN;
+  double acc[MT][2];
+  int I[MT], J[MT];
+#pragma unroll
+  for (int q = 0; q < MT; q++) {
+    const int tile = warp + q * (NT / 32);
+    I[q] = tile / TN;
+    J[q] = tile - I[q] * TN;
+    acc[q][0] = acc[q][1] = 0.0;
+  }
+  for (int k = 0; k < K; k += 4) {
+#pragma unroll
+    for (int q = 0; q < MT; q++)
+      if (warp + q * (NT / 32) < ntile)
+        dmma884(acc[q], A[(8 * I[q] + g8) * lda + k + tq], B[(k + tq) * ldb + 8 * J[q] + g8]);
+  }
+#pragma unroll
+  for (int q = 0; q < MT; q++) {
+    if (warp + q * (NT / 32) >= ntile) continue;
+    double* c = C + (8 * I[q] + g8) * ldc + 8 * J[q] + 2 * tq;
+    c[0] = alpha * acc[q][0];
+    c[1] = alpha * acc[q][1];
+  }
+}
+
+template <int NT>
+__device__ void diag64_smem(double (*D)[DLD], double (*Mi)[DLD], double* dv, int kb) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, tq = lane & 3;
+  const int npan = (kb + 15) >> 4;
+#pragma unroll 1
+  for (int p = 0; p < 4; p++) {
+    const int c0 = 16 * p;
+    if (p < npan) {
+      if (warp == 0) panel16_warp(D, dv, c0, lane);
+    } else if (tid < 16) {
+      dv[c0 + tid] = 1.0;  // unit padding
+    }
+    __syncthreads();
+    TFB_PHASE(2 + 2 * p);
+    // rank-16 DMMA update of the trailing lower block [c0+16, 64)
+    const int t0 = c0 + 16;
+    if (p + 1 < npan) {
+      // every warp keeps its (<= MT) tiles' accumulators live so the DMMA
+      // chains interleave instead of serialising on one accumulator
+      const int T = (NB - t0) >> 3, ntile = T * (T + 1) / 2;
+      constexpr int MT = (21 + NT / 32 - 1) / (NT / 32);
+      double acc[MT][2];
+      int ra[MT], rb[MT];
+#pragma unroll
+      for (int q = 0; q < MT; q++) {
+        const int tile = warp + q * (NT / 32);
+        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+        I -= (I * (I + 1) / 2 > tile);
+        I += ((I + 1) * (I + 2) / 2 <= tile);
+        const int J = tile - I * (I + 1) / 2;
+        ra[q] = t0 + 8 * I + g8;
+        rb[q] = t0 + 8 * J + g8;
+        acc[q][0] = acc[q][1] = 0.0;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4) {
+        const int qc = c0 + kk + tq;
+        const double dq = dv[qc];
+#pragma unroll
+        for (int q = 0; q < MT; q++)
+          if (warp + q * (NT / 32) < ntile) dmma884(acc[q], D[ra[q]][qc] * dq, D[rb[q]][qc]);
+      }
+#pragma unroll
+      for (int q = 0; q < MT; q++) {
+        if (warp + q * (NT / 32) >= ntile) continue;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cc = (rb[q] - g8) + 2 * tq + h;
+          if (cc <= ra[q]) D[ra[q]][cc] -= acc[q][h];
+        }
+      }
+      __syncthreads();
+      TFB_PHASE(3 + 2 * p);
+    }
+  }
+  // M = L^-1 by recursive doubling: 16x16 diagonal-block inverses (half-warps,
+  // registers + width-16 shuffles), then M21 = -M22 (L21 M11) at the 32- and
+  // 64-levels as DMMA products (scratch: upper part of Mi, cleared after use).
+  if (warp < 2) inv16_half(D, Mi, 16 * (2 * warp + (lane >> 4)), lane & 15);
+  __syncthreads();
+  TFB_PHASE(10);
+  smem_gemm<NT, (4 + NT / 32 - 1) / (NT / 32)>(&Mi[0][16], DLD, &D[16][0], DLD, &Mi[0][0], DLD, 16, 16, 16, 1.0);
+  smem_gemm<NT, (4 + NT / 32 - 1) / (NT / 32)>(&Mi[32][48], DLD, &D[48][32], DLD, &Mi[32][32], DLD, 16, 16, 16, 1.0);
+  __syncthreads();
+  smem_gemm<NT, (4 + NT / 32 - 1) / (NT / 32)>(&Mi[16][0], DLD, &Mi[16][16], DLD, &Mi[0][16], DLD, 16, 16, 16, -1.0);
+  smem_gemm<NT, (4 + NT / 32 - 1) / (NT / 32)>(&Mi[48][32], DLD, &Mi[48][48], DLD, &Mi[32][48], DLD, 16, 16, 16, -1.0);
+  __syncthreads();
+  for (int e = tid; e < 2 * 256; e += NT) {
+    const int o = (e >> 8) * 32, r = (e >> 4) & 15, c = e & 15;
+    Mi[o + r][o + 16 + c] = 0.0;
+  }
+  __syncthreads();
+  TFB_PHASE(11);
+  if (kb > 32) {
+    smem_gemm<NT, (16 + NT / 32 - 1) / (NT / 32)>(&Mi[0][32], DLD, &D[32][0], DLD, &Mi[0][0], DLD, 32, 32, 32, 1.0);
+    __syncthreads();
+    smem_gemm<NT, (16 + NT / 32 - 1) / (NT / 32)>(&Mi[32][0], DLD, &Mi[32][32], DLD, &Mi[0][32], DLD, 32, 32, 32, -1.0);
+  } else {
+    for (int e = tid; e < 32 * 32; e += NT) Mi[32 + (e >> 5)][e & 31] = 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < 32 * 32; e += NT) Mi[e >> 5][32 + (e & 31)] = 0.0;
+  __syncthreads();
+  TFB_PHASE(12);
+}
+
+// aux block: strict lower = M, diagonal = d (1 beyond kb), strict upper = l^T.
+template <int NT>
+__device__ __forceinline__ void write_aux64(double* M, double (*D)[DLD], double (*Mi)[DLD],
+                                            const double* dv, int kb) {
+  for (int e = threadIdx.x; e < NB * NB; e += NT) {
+    const int i = e >> 6, j = e & 63;
+    M[e] = j < i ? Mi[i][j] : (j == i ? (i < kb ? dv[i] : 1.0) : (j < kb ? D[j][i] : 0.0));
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void load_diag_block(double (*D)[DLD], const double* Pf, int kp, int a,
+                                                int kb) {
+  // every load of the block in flight before the first shared-memory store
+  constexpr int Q = NB * NB / NT;
+  double t[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int e = threadIdx.x + q * NT, i = e >> 6, j = e & 63;
+    t[q] = (i < kb && j <= i) ? Pf[(long long)(a + i) * kp + a + j] : (i == j ? 1.0 : 0.0);
+  }
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int e = threadIdx.x + q * NT;
+    D[e >> 6][e & 63] = t[q];
+  }
+}
+
+constexpr size_t kDiagSmem = sizeof(double) * (2 * NB * DLD + NB);
+
+// One CTA per front: diagonal blocks of width kb in (32, 64].  Writes l and d
+// into the panel, d into the pivot vector, and the aux block.
+__global__ void __launch_bounds__(256) large_diag64_kernel(LevelArgs L, double* factors, int a,
+                                                            double threshold,
+                                                            unsigned long long* err) {
+  extern __shared__ __align__(16) double dsm[];
+  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(dsm);
+  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(dsm + NB * DLD);
+  double* dv = dsm + 2 * NB * DLD;
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(a + NB, s.k) - a;
   if (kb <= 0) return;
   double* Pf = factors + f * L.fac_stride;
-  const int tid = threadIdx.x, r = tid / Q, h = tid % Q, c0 = h * W;
-  const int lane = tid & 31, quad = lane & ~(Q - 1);
-  double v[W];
-#pragma unroll
-  for (int j = 0; j < W; j++) {
-    const int col = c0 + j;
-    v[j] = (r < kb && col <= r) ? Pf[(long long)(a + r) * s.kp + a + col] : (r == col ? 1.0 : 0.0);
-  }
-  const long long piv0 = L.piv_off[f] + a;
-  // LDL^T: a(r,s) -= (a(s,c)/d) a(r,c); column c becomes l(r,c) = a(r,c)/d.
-  // The pivot loop stays rolled (straight-line code executed once per CTA
-  // would miss the instruction cache); register slots are selected by
-  // compile-time indices inside the unrolled inner loops.
-#pragma unroll 1
-  for (int c = 0; c < kb; c++) {
-    double* cb = buf[c & 1];
-    const int cj = c % W;
-    const bool own = h == c / W;
-    if (own && r >= c) {
-      double vc = 0.0;
-#pragma unroll
-      for (int j = 0; j < W; j++) vc = (j == cj) ? v[j] : vc;
-      cb[r] = vc;
-    }
-    __syncthreads();
-    const double d = cb[c];
-    if (tid == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-    const double inv = 1.0 / d;
-    if (r > c && r < kb) {
-      const double arc = cb[r];
-#pragma unroll
-      for (int j = 0; j < W; j++) {
-        const int col = c0 + j;
-        if (col > c && col <= r) v[j] -= (cb[col] * inv) * arc;
-        if (own && j == cj) v[j] = arc * inv;
-      }
-    }
-  }
-  // write l (strict lower) and d back
-  if (r < kb) {
-#pragma unroll
-    for (int j = 0; j < W; j++) {
-      const int col = c0 + j;
-      if (col <= r) Pf[(long long)(a + r) * s.kp + a + col] = v[j];
-      if (col == r) Pf[(long long)s.m * s.kp + a + r] = v[j];
-    }
-  }
-  // unit-lower inverse M = L^-1, right-looking over rows t of M
-  double w[W];
-#pragma unroll
-  for (int j = 0; j < W; j++) w[j] = (c0 + j == r) ? 1.0 : 0.0;
+  TFB_PHASE(0);
+  load_diag_block<256>(D, Pf, s.kp, a, kb);
   __syncthreads();
-#pragma unroll 1
-  for (int t = 0; t < kb - 1; t++) {
-    double* rb = buf[t & 1];
-    if (r == t) {
-#pragma unroll
-      for (int j = 0; j < W; j++) rb[c0 + j] = w[j];
-    }
-    __syncthreads();
-    // L[r][t] lives in the quad lane owning column block t / W
-    const int tj = t % W;
-    double vt = 0.0;
-#pragma unroll
-    for (int j = 0; j < W; j++) vt = (j == tj) ? v[j] : vt;
-    const double lrt = __shfl_sync(0xffffffffu, vt, quad | (t / W));
-    if (r > t && r < kb) {
-#pragma unroll
-      for (int j = 0; j < W; j++)
-        if (c0 + j <= t) w[j] -= lrt * rb[c0 + j];
-    }
+  TFB_PHASE(1);
+  diag64_smem<256>(D, Mi, dv, kb);
+  for (int e = threadIdx.x; e < NB * NB; e += 256) {
+    const int i = e >> 6, j = e & 63;
+    if (i < kb && j <= i) Pf[(long long)(a + i) * s.kp + a + j] = D[i][j];
   }
-  // aux block: strict lower = M, diagonal = d, strict upper = l transposed
-  double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
-#pragma unroll
-  for (int j = 0; j < W; j++) {
-    const int col = c0 + j;
-    if (col < r) {
-      M[r * NB + col] = w[j];
-      M[col * NB + r] = r < kb ? v[j] : 0.0;
-    } else if (col == r) {
-      M[r * NB + r] = r < kb ? v[j] : 1.0;
-    }
+  for (int c = threadIdx.x; c < kb; c += 256) {
+    Pf[(long long)s.m * s.kp + a + c] = dv[c];
+    if (fabs(dv[c]) <= threshold) record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + a + c));
   }
+  write_aux64<256>(L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB, D, Mi, dv, kb);
+  TFB_PHASE(13);
 }
 
 // One 64-wide diagonal block of every front's panel, fused with the triangular
 // solve of the rows below it.  grid = (fronts, row tiles of 64).  Every CTA
-// factors the diagonal block redundantly in shared memory (blocked LDL^T:
-// 16-column panels with rank-1 steps, DMMA rank-16 trailing updates), forms
-// its unit-lower inverse M (inverted 16x16 diagonal blocks + block
-// substitution), then solves its 64-row tile as a DMMA product
-// P_rb <- (P_rb M^T) D^-1.  The CTA of row tile 0 also writes l, d and M.
+// factors the diagonal block redundantly (diag64_smem), then solves its 64-row
+// tile as a DMMA product P_rb <- (P_rb M^T) D^-1.  The CTA of row tile 0 also
+// writes d and the aux block.
 constexpr int TRB = 64;
 constexpr int kFusedBlockMaxFronts = 2;
-constexpr int DLD = NB + 1, ALD = NB + 4;
-constexpr size_t kBlockSmem = sizeof(double) * (2 * NB * DLD + TRB * ALD + 2 * NB);
+constexpr int ALD = NB + 4;
+constexpr size_t kBlockSmem = sizeof(double) * (2 * NB * DLD + TRB * ALD + NB);
 
 __global__ void __launch_bounds__(256) large_block_kernel(LevelArgs L, double* factors, int a,
                                                            double threshold,
@@ -188,7 +454,6 @@ __global__ void __launch_bounds__(256) large_block_kernel(LevelArgs L, double* f
   double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(bsm + NB * DLD);
   double(*At)[ALD] = reinterpret_cast<double(*)[ALD]>(bsm + 2 * NB * DLD);
   double* dv = bsm + 2 * NB * DLD + TRB * ALD;
-  double* lv = dv + NB;
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const int kb = min(a + NB, s.k) - a;
@@ -200,119 +465,28 @@ __global__ void __launch_bounds__(256) large_block_kernel(LevelArgs L, double* f
   double* Pf = factors + f * L.fac_stride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, tq = lane & 3;
 
-  // 1. diagonal block (identity pad beyond kb) and this CTA's row tile
-  for (int e = tid; e < NB * NB; e += 256) {
+  // 1. diagonal block (unit rows beyond kb) and this CTA's row tile
+  load_diag_block<256>(D, Pf, s.kp, a, kb);
+  for (int e = tid; e < TRB * NB; e += 256) {
     const int i = e >> 6, j = e & 63;
-    D[i][j] = (i < kb && j <= i) ? Pf[(long long)(a + i) * s.kp + a + j] : (i == j ? 1.0 : 0.0);
     At[i][j] = (i < rows && j < kb) ? Pf[(long long)(row0 + i) * s.kp + a + j] : 0.0;
   }
   __syncthreads();
-
-  // 2. blocked LDL^T of D
-  const long long piv0 = L.piv_off[f] + a;
-  for (int c0 = 0; c0 < kb; c0 += 16) {
-    const int c1 = min(c0 + 16, kb);
-    for (int c = c0; c < c1; c++) {
-      const double d = D[c][c];
-      if (writer && tid == 0 && fabs(d) <= threshold)
-        record_zero_pivot(err, (unsigned long long)(piv0 + c));
-      if (tid > c && tid < NB) {
-        const double l = D[tid][c] / d;
-        lv[tid] = l;
-        D[tid][c] = l;
-      }
-      if (tid == c) dv[c] = d;
-      __syncthreads();
-      const int nc = c1 - c - 1;
-      if (nc > 0) {
-        const int n = (NB - c - 1) * nc;
-        for (int e = tid; e < n; e += 256) {
-          const int r = c + 1 + e / nc, q = c + 1 + e % nc;
-          if (q <= r) D[r][q] -= lv[q] * (lv[r] * d);
-        }
-      }
-      __syncthreads();
-    }
-    // rank-(c1-c0) DMMA update of the trailing columns [c0+16, 64)
-    const int t0 = c0 + 16;
-    if (t0 < NB) {
-      const int T = (NB - t0) >> 3, ntile = T * (T + 1) / 2;
-      for (int tile = warp; tile < ntile; tile += 8) {
-        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-        while (I * (I + 1) / 2 > tile) I--;
-        while ((I + 1) * (I + 2) / 2 <= tile) I++;
-        const int J = tile - I * (I + 1) / 2;
-        const int ra = t0 + 8 * I + g8, rb = t0 + 8 * J + g8;
-        double acc[2] = {0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 16; kk += 4) {
-          const int q = c0 + kk + tq;
-          const bool v = q < c1;
-          dmma884(acc, v ? D[ra][q] * dv[q] : 0.0, v ? D[rb][q] : 0.0);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int cc = t0 + 8 * J + 2 * tq + h;
-          if (cc <= ra) D[ra][cc] -= acc[h];
-        }
-      }
-    }
-    __syncthreads();
-  }
-
-  // 3. M = L^-1: 16x16 diagonal blocks (warp w < 4, lane c < 16 owns column c) ...
-  if (warp < 4 && lane < 16) {
-    const int o = warp * 16, c = lane;
-    for (int r = 0; r < 16; r++) Mi[o + r][o + c] = r == c ? 1.0 : 0.0;
-    for (int r = c + 1; r < 16; r++) {
-      double acc = 0.0;
-      for (int t = c; t < r; t++) acc -= D[o + r][o + t] * Mi[o + t][o + c];
-      Mi[o + r][o + c] = acc;
-    }
-  }
-  __syncthreads();
-  // ... then block rows: M_ij = -M_ii * sum_{t=j}^{i-1} L_it M_tj
-  for (int bi = 1; bi < 4; bi++) {
-    const int oi = 16 * bi;
-    // S_ij into lv-free scratch: reuse At? no -- use the upper triangle of Mi as scratch
-    for (int e = tid; e < bi * 256; e += 256) {
-      const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const int oj = 16 * bj;
-      double acc = 0.0;
-      for (int t = oj; t < oi; t++) acc += D[oi + r][t] * Mi[t][oj + c];
-      Mi[oj + c][oi + r] = acc;  // scratch: upper part, transposed
-    }
-    __syncthreads();
-    for (int e = tid; e < bi * 256; e += 256) {
-      const int bj = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const int oj = 16 * bj;
-      double acc = 0.0;
-      for (int t = 0; t <= r; t++) acc -= Mi[oi + r][oi + t] * Mi[oj + c][oi + t];
-      Mi[oi + r][oj + c] = acc;
-    }
-    __syncthreads();
-  }
-  // clear the scratch (upper part) so M is exactly lower-triangular
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int i = e >> 6, j = e & 63;
-    if (j > i) Mi[i][j] = 0.0;
-  }
-  __syncthreads();
-
-  // 4. write d and the aux block: strict lower = M, diagonal = d, strict upper =
-  // l transposed.  The panel's own diagonal block is not rewritten here: other
-  // CTAs of this launch may still be reading its assembled values, so
-  // large_diag_finalize_kernel copies l, d into it after the level.
+  // 2. factor + invert the diagonal block
+  diag64_smem<256>(D, Mi, dv, kb);
+  // 3. the writer CTA stores d and the aux block.  The panel's own diagonal
+  // block is not rewritten here: other CTAs of this launch may still be
+  // reading its assembled values, so large_diag_finalize_kernel copies l, d
+  // into it after the level.
   if (writer) {
-    for (int c = tid; c < kb; c += 256) Pf[(long long)s.m * s.kp + a + c] = dv[c];
-    double* M = L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB;
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int i = e >> 6, j = e & 63;
-      M[e] = j < i ? Mi[i][j] : (j == i ? (i < kb ? dv[i] : 1.0) : (j < kb ? D[j][i] : 0.0));
+    for (int c = tid; c < kb; c += 256) {
+      Pf[(long long)s.m * s.kp + a + c] = dv[c];
+      if (fabs(dv[c]) <= threshold)
+        record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + a + c));
     }
+    write_aux64<256>(L.aux + f * L.aux_stride + (long long)(a / NB) * NB * NB, D, Mi, dv, kb);
   }
-
-  // 5. row tile: X = At M^T, then column c / d_c (DMMA, 8 tiles of 8x8 per warp)
+  // 4. row tile: X = At M^T, then column c / d_c (DMMA, 8 tiles of 8x8 per warp)
   if (rows > 0) {
     for (int tile = warp; tile < 64; tile += 8) {
       const int I = tile >> 3, J = tile & 7;
@@ -578,7 +752,10 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
     } else {
       // many fronts: register-tiled diagonal blocks, then the TRSM as a DMMA GEMM
       timer_begin(K_DIAG, st);
-      large_diag_kernel<<<L.n_fronts, 256, 0, st>>>(L, factors, a, thr, err);
+      if (std::min(NB, L.max_k - a) <= 32)
+        large_diag32_kernel<<<(L.n_fronts + 3) / 4, 128, 0, st>>>(L, factors, a, thr, err);
+      else
+        large_diag64_kernel<<<L.n_fronts, 256, kDiagSmem, st>>>(L, factors, a, thr, err);
       timer_end(st);
       dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GTrsm::BM - 1) / GTrsm::BM));
       gemm_attr<2, GTrsm>();
@@ -615,13 +792,20 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   if (!attr) {
     cudaFuncSetAttribute(large_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBlockSmem);
+    cudaFuncSetAttribute(large_diag64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDiagSmem);
     attr = true;
   }
   {
-    const long long per = L.fac_stride + tri(L.max_upd, 0);
-    const unsigned gx = (unsigned)std::min<long long>((per + 255) / 256, 1024);
+    // ~kAsmRowsPerWarp rows per warp, but at least ~8 CTAs per SM on levels
+    // with few (large) fronts, down to one row per warp
+    const long long by_rows = (L.max_m + kAsmWarps * kAsmRowsPerWarp - 1) / (kAsmWarps * kAsmRowsPerWarp);
+    const long long by_sms = (148LL * 8 + L.n_fronts - 1) / L.n_fronts;
+    const long long cap = (L.max_m + kAsmWarps - 1) / kAsmWarps;
+    const unsigned gy = (unsigned)std::max(1LL, std::min(std::max(by_rows, by_sms), cap));
     timer_begin(K_ASSEMBLE, st);
-    large_assemble_kernel<<<dim3(L.n_fronts, gx), 256, 0, st>>>(L, child_upd, factors, upd_out);
+    large_assemble_kernel<<<dim3(L.n_fronts, gy), 32 * kAsmWarps, 0, st>>>(L, child_upd, factors,
+                                                                           upd_out);
     timer_end(st);
   }
   cudaError_t e = cudaGetLastError();

@@ -44,13 +44,32 @@ def run_levels():
 for r in range(a.reps):
     times = run_levels()
 assert dp.zero_pivot_position() == -1
+# per-level kernel-class breakdown (events around every launch)
+lib.tf_timing_enable(1)
+_lib.kernel_timing(lib)
+cls_rows = []
+dp.err.fill_(-1)
+prev = None
+sp0 = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+for L, dl in enumerate(dp.levels):
+    out = dp.upd[L & 1]
+    assert lib.tf_level_factor(C.byref(dl.view), None if prev is None else C.c_void_p(prev.data_ptr()),
+                               C.c_void_p(dp.elem.data_ptr()), C.c_void_p(dp.factors[L].data_ptr()),
+                               C.c_void_p(out.data_ptr()), C.c_double(state.zero_threshold),
+                               C.c_void_p(dp.err.data_ptr()), None, 0, sp0) == 0
+    prev = out
+    torch.cuda.synchronize()
+    cls_rows.append(_lib.kernel_timing(lib))
+lib.tf_timing_enable(0)
 tot = sum(times)
 print(f"factor total {tot:.3f} ms")
 for L, (t, s) in enumerate(zip(times, stats)):
-    gfs = s["ldl_flops"] / t / 1e9 if t > 0 else 0
+    gfs = s["ldl_flops"] / t / 1e6 if t > 0 else 0
     gbs = s["bytes"] / t / 1e6 if t > 0 else 0
     print(f"L{L:2d} fronts={s['fronts']:9d} m={s['max_m']:5d} k={s['max_k']:5d} t={t:8.3f}ms "
           f"{gfs/1e3:7.2f} TF/s {gbs:8.1f} GB/s")
+    print("      " + "  ".join(f"{k.split(' ')[0].replace('large_', '')[:14]}{k.split(' ')[-1] if '(' in k else ''}"
+                              f"={v[0]:.3f}/{v[1]}" for k, v in cls_rows[L].items()))
 b = torch.randn(mesh.n_dof, a.nrhs, dtype=torch.float64, device="cuda")
 x = torch.empty_like(b)
 for r in range(a.reps):
