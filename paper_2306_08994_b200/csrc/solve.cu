@@ -50,12 +50,28 @@ __device__ __forceinline__ void stage_panel(double* Ls, const double* __restrict
 }
 
 // Vectors: row stride ldr (total RHS columns); this launch handles columns
-// [col0, col0 + nr).  Front blocks in w_in / w_out have the same row stride.
-template <int G, int GPC>
+// [col0, col0 + nr).  With one column (nr == 1) every panel entry is used
+// exactly once, so the panel is read straight from global memory and shared
+// memory holds only the front's vector block (high occupancy); with several
+// columns the panel is staged once and reused across them.
+// Block conventions: the forward sweep of a small level writes a front's
+// update rows only, at rows [0, m-k) of its block (no child-shape lookup for
+// the parent); large levels work in place (update rows at [k, m)).  The
+// backward sweep writes all m rows.
+template <bool STAGE>
+struct PanelRef {
+  const double* p;
+  int ld;
+  __device__ __forceinline__ double operator()(int r, int c) const {
+    return STAGE ? p[r * ld + c] : __ldg(p + (long long)r * ld + c);
+  }
+};
+
+template <int G, int GPC, bool STAGE>
 __global__ void __launch_bounds__(G* GPC)
     solve_fwd_small(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
-                    const double* __restrict__ w_child, long long child_rows, double* w_out,
-                    long long out_rows, double* y, int nr, int ldr, int col0,
+                    const double* __restrict__ w_child, long long child_rows, int child_at0,
+                    double* w_out, long long out_rows, double* y, int nr, int ldr, int col0,
                     int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
@@ -65,9 +81,15 @@ __global__ void __launch_bounds__(G* GPC)
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
-  double* Ls = W + L.max_m * nr;  // panel staged in shared memory: Ls[r*k + c], then d
-  stage_panel<G>(Ls, factors + f * L.fac_stride, m, k, kp, t);
-  const double* Lp = Ls;
+  const double* Pg = factors + f * L.fac_stride;
+  PanelRef<STAGE> Lp{Pg, kp};
+  const double* dv = Pg + (long long)m * kp;
+  if (STAGE) {
+    double* Ls = W + L.max_m * nr;  // panel staged in shared memory: Ls[r*k + c], then d
+    stage_panel<G>(Ls, Pg, m, k, kp, t);
+    Lp = PanelRef<STAGE>{Ls, k};
+    dv = Ls + m * k;
+  }
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nW; e += G) {
     const int r = e / nr, j = e - r * nr;
@@ -77,10 +99,11 @@ __global__ void __launch_bounds__(G* GPC)
   if (!L.is_leaf) {
     for (int c = 0; c < s.nsrc; c++) {
       const long long ch = 2 * (L.front_base + f) + c - C.front_base;
-      const int kc = C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
+      const int off =
+          child_at0 ? 0 : C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
       const int len = c == 0 ? s.len0 : s.len1;
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
-      const double* Wc = w_child + (ch * child_rows + kc) * ldr + col0;
+      const double* Wc = w_child + (ch * child_rows + off) * ldr + col0;
       const int n = len * nr;
       for (int e = t; e < n; e += G) {
         const int a = e / nr, j = e - a * nr;
@@ -89,28 +112,31 @@ __global__ void __launch_bounds__(G* GPC)
       group_sync<G>(bar);
     }
   }
+  // pivot block: right-looking inside the k x k triangle
   for (int c = 0; c < k; c++) {
-    const int n = (m - c - 1) * nr;
+    const int n = (k - c - 1) * nr;
     const double* Wc = W + c * nr;
     for (int e = t; e < n; e += G) {
       const int r = c + 1 + e / nr, j = e % nr;
-      W[r * nr + j] -= Lp[r * k + c] * Wc[j];
+      W[r * nr + j] -= Lp(r, c) * Wc[j];
     }
     group_sync<G>(bar);
   }
-  const double* dv = Lp + m * k;
   for (int e = t; e < nK; e += G) {
     const int r = e / nr, j = e - r * nr;
     y[(piv + r) * ldr + col0 + j] = W[e] / dv[r];
   }
+  // update rows: w_r - l_r . w_piv (row-contiguous panel reads), straight out
   double* out = w_out + f * out_rows * ldr + col0;
   for (int e = nK + t; e < nW; e += G) {
     const int r = e / nr, j = e - r * nr;
-    out[(long long)r * ldr + j] = W[e];
+    double acc = W[e];
+    for (int c = 0; c < k; c++) acc -= Lp(r, c) * W[c * nr + j];
+    out[(long long)(r - k) * ldr + j] = acc;
   }
 }
 
-template <int G, int GPC>
+template <int G, int GPC, bool STAGE>
 __global__ void __launch_bounds__(G* GPC)
     solve_bwd_small(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
                     const double* __restrict__ x_parent, long long parent_rows, double* x_out,
@@ -124,9 +150,13 @@ __global__ void __launch_bounds__(G* GPC)
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   const long long piv = L.piv_off[f];
-  double* Ls = X + L.max_m * nr;
-  stage_panel<G>(Ls, factors + f * L.fac_stride, m, k, kp, t);
-  const double* Lp = Ls;
+  const double* Pg = factors + f * L.fac_stride;
+  PanelRef<STAGE> Lp{Pg, kp};
+  if (STAGE) {
+    double* Ls = X + L.max_m * nr;
+    stage_panel<G>(Ls, Pg, m, k, kp, t);
+    Lp = PanelRef<STAGE>{Ls, k};
+  }
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nK; e += G) {
     const int r = e / nr, j = e - r * nr;
@@ -148,7 +178,7 @@ __global__ void __launch_bounds__(G* GPC)
     for (int e = t; e < nK; e += G) {
       const int c = e / nr, j = e - c * nr;
       double acc = X[e];
-      for (int r = k; r < m; r++) acc -= Lp[r * k + c] * X[r * nr + j];
+      for (int r = k; r < m; r++) acc -= Lp(r, c) * X[r * nr + j];
       X[e] = acc;
     }
     group_sync<G>(bar);
@@ -158,7 +188,7 @@ __global__ void __launch_bounds__(G* GPC)
     const int n = c * nr;
     for (int e = t; e < n; e += G) {
       const int r = e / nr, j = e - r * nr;
-      X[e] -= Lp[c * k + r] * Xc[j];
+      X[e] -= Lp(c, r) * Xc[j];
     }
     group_sync<G>(bar);
   }
@@ -177,15 +207,17 @@ __global__ void __launch_bounds__(G* GPC)
 
 // ------------------------------------------------------------- large fronts
 __global__ void solve_gather_fwd(LevelArgs L, LevelArgs C, const double* __restrict__ w_child,
-                                 long long child_rows, double* W, long long out_rows,
-                                 const double* __restrict__ y, int nrhs) {
+                                 long long child_rows, int child_at0, double* W,
+                                 long long out_rows, const double* __restrict__ y, int nrhs) {
   const long long f = blockIdx.x;
   const Shape s = front_shape(L, f);
   const long long piv = L.piv_off[f];
   const int nW = s.m * nrhs, nK = s.k * nrhs;
   int kc[2] = {0, 0};
-  for (int c = 0; c < s.nsrc; c++)
-    kc[c] = C.pat[(size_t)C.pattern_of[2 * (L.front_base + f) + c - C.front_base] * TF_PAT_WIDTH + TF_PAT_K];
+  for (int c = 0; c < s.nsrc; c++)  // update rows of a small child's block start at 0
+    kc[c] = child_at0 ? 0
+                      : C.pat[(size_t)C.pattern_of[2 * (L.front_base + f) + c - C.front_base] *
+                                  TF_PAT_WIDTH + TF_PAT_K];
   double* Wf = W + f * out_rows * nrhs;
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {
     const int r = e / nrhs, j = e - r * nrhs;
@@ -383,24 +415,25 @@ __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
 // ------------------------------------------------------------------ launch
 constexpr size_t kSmallSolveSmem = 160 * 1024;
 
-template <int G, int GPC, bool FWD>
+template <int G, int GPC, bool FWD, bool STAGE>
 static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, int flag,
                                       const double* factors, const double* w_in,
                                       long long in_rows, double* w_out, long long out_rows,
                                       double* y, int nr, int ldr, int col0, cudaStream_t st) {
-  const int per = (int)(((size_t)(L.max_m * nr + L.max_m * L.max_k + L.max_m) * 8 + 15) & ~(size_t)15);
+  const size_t pan = STAGE ? (size_t)L.max_m * L.max_k + L.max_m : 0;
+  const int per = (int)(((size_t)L.max_m * nr + pan) * 8 + 15) & ~15;
   const size_t smem = (size_t)per * GPC;
   const unsigned blocks = (unsigned)((L.n_fronts + GPC - 1) / GPC);
   if (FWD) {
-    auto kern = solve_fwd_small<G, GPC>;
+    auto kern = solve_fwd_small<G, GPC, STAGE>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     timer_begin(K_SOLVE_SMALL_FWD, st);
-    kern<<<blocks, G * GPC, smem, st>>>(L, O, factors, w_in, in_rows, w_out, out_rows, y, nr, ldr,
-                                        col0, per);
+    kern<<<blocks, G * GPC, smem, st>>>(L, O, factors, w_in, in_rows, flag, w_out, out_rows, y,
+                                        nr, ldr, col0, per);
     timer_end(st);
   } else {
-    auto kern = solve_bwd_small<G, GPC>;
+    auto kern = solve_bwd_small<G, GPC, STAGE>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     timer_begin(K_SOLVE_SMALL_BWD, st);
@@ -417,6 +450,8 @@ static int small_cols(const LevelArgs& L, int nrhs) {
   return std::max(1, std::min(nrhs, cmax));
 }
 
+// flag: forward -- 1 if the child level's update rows start at row 0 of its
+// blocks (small child level); backward -- has_parent.
 template <bool FWD>
 static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int flag,
                                   const double* factors, const double* w_in, long long in_rows,
@@ -426,20 +461,31 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
     const long long work = (long long)L.max_m * nr;
-    const long long bytes = (work + (long long)L.max_m * L.max_k + L.max_m) * 8;
     cudaError_t e;
-#define TFB_SMALL(G, GPC)                                                                  \
-  launch_small_solve<G, GPC, FWD>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nr, \
-                                  nrhs, col0, st)
-    if (work <= 12 && bytes * 128 <= (long long)kSmallSolveSmem) e = TFB_SMALL(1, 128);
-    else if (work <= 24 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(2, 64);
-    else if (work <= 48 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(4, 64);
-    else if (work <= 96 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
-    else if (work <= 64 && bytes * 16 <= (long long)kSmallSolveSmem) e = TFB_SMALL(16, 16);
-    else if (work <= 256 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
-    else if (work <= 2048 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
-    else e = TFB_SMALL(256, 1);
+    if (nr == 1) {  // vector block only in shared memory
+#define TFB_SMALL(G, GPC)                                                                    \
+  launch_small_solve<G, GPC, FWD, false>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, \
+                                         y, nr, nrhs, col0, st)
+      if (work <= 12) e = TFB_SMALL(1, 128);
+      else if (work <= 24) e = TFB_SMALL(2, 64);
+      else if (work <= 48) e = TFB_SMALL(4, 64);
+      else if (work <= 96) e = TFB_SMALL(8, 32);
+      else if (work <= 256) e = TFB_SMALL(32, 8);
+      else e = TFB_SMALL(128, 2);
 #undef TFB_SMALL
+    } else {
+      const long long bytes = (work + (long long)L.max_m * L.max_k + L.max_m) * 8;
+#define TFB_SMALL(G, GPC)                                                                   \
+  launch_small_solve<G, GPC, FWD, true>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, \
+                                        y, nr, nrhs, col0, st)
+      if (work <= 24 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(2, 64);
+      else if (work <= 48 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(4, 64);
+      else if (work <= 96 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
+      else if (work <= 256 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
+      else if (work <= 2048 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
+      else e = TFB_SMALL(256, 1);
+#undef TFB_SMALL
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -455,13 +501,14 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
                              const double* w_child, long long child_rows, double* w_out,
                              long long out_rows, double* y, int nrhs, cudaStream_t st) {
   if (!level_is_large(L.is_leaf, L.max_m))
-    return dispatch_small<true>(L, C, 0, factors, w_child, child_rows, w_out, out_rows, y, nrhs,
-                                st);
+    return dispatch_small<true>(L, C, level_is_large(C.is_leaf, C.max_m) ? 0 : 1, factors, w_child,
+                                child_rows, w_out, out_rows, y, nrhs, st);
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
   timer_begin(K_SOLVE_GATHER, st);
   solve_gather_fwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
-                     st>>>(L, C, w_child, child_rows, w_out, out_rows, y, nrhs);
+                     st>>>(L, C, w_child, child_rows, level_is_large(C.is_leaf, C.max_m) ? 0 : 1, w_out, out_rows, y,
+                          nrhs);
   timer_end(st);
   const size_t smem = sizeof(double) * (2 * SB * (size_t)nrhs + SB * SB);
   cudaFuncSetAttribute(solve_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
