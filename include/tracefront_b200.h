@@ -173,13 +173,17 @@ int tf_subtree_factor(const tf_level_view* views, int32_t nlev, double* const* f
 
 /* Forward sweep of solve (engine.py:481-487) for one level, nrhs columns,
  * row-major (n x nrhs) vectors in pivot order.  child: view of level-1 (NULL
- * at the leaves); w_child: its front blocks (stride child_rows * nrhs, update
- * rows start at the child's k); w_out: this level's front blocks (stride
- * out_rows * nrhs, out_rows >= max_m); y: pivot-order RHS, overwritten by
- * D^-1 L^-1 b at this level's pivots. */
+ * at the leaves); w_child: its front blocks (stride child_rows * nrhs);
+ * w_out: this level's front blocks (stride out_rows * nrhs, out_rows >=
+ * max_m).  A front's update rows are left in its block at rows [0, m-k) on
+ * shared-memory levels and in place at rows [k, m) on large-front levels;
+ * y: pivot-order RHS, overwritten by D^-1 L^-1 b at this level's pivots.
+ * workspace: tf_level_solve_workspace bytes (flags + blocks of the
+ * wavefront sweep on large-front levels; 0 bytes otherwise). */
 int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,
                        const double* factors, const double* w_child, int64_t child_rows,
-                       double* w_out, int64_t out_rows, double* y, int32_t nrhs, void* stream);
+                       double* w_out, int64_t out_rows, double* y, int32_t nrhs,
+                       void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Backward sweep (engine.py:488-492) for one level.  parent: view of
  * level+1 (NULL at the root level) and its x buffer (stride parent_rows*nrhs);
@@ -190,7 +194,7 @@ int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
                        double* x_out, int64_t out_rows, double* y, int32_t nrhs,
                        void* workspace, int64_t workspace_bytes, void* stream);
 
-/* Workspace bytes tf_level_solve_bwd needs for this level and nrhs. */
+/* Workspace bytes tf_level_solve_fwd / tf_level_solve_bwd need for this level and nrhs. */
 int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs);
 
 /* out[i, :] = in[idx[i]-1, :] (natural -> pivot order); inverse when scatter != 0. */

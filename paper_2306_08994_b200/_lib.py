@@ -108,7 +108,7 @@ def load() -> C.CDLL:
                                     i64, vp]
     lib.tf_level_factor.restype = C.c_int
     lib.tf_level_solve_fwd.argtypes = [C.POINTER(LevelView), C.POINTER(LevelView), vp, vp, i64,
-                                       vp, i64, vp, i32, vp]
+                                       vp, i64, vp, i32, vp, i64, vp]
     lib.tf_level_solve_fwd.restype = C.c_int
     lib.tf_level_solve_bwd.argtypes = [C.POINTER(LevelView), C.POINTER(LevelView), vp, vp, i64,
                                        vp, i64, vp, i32, vp, i64, vp]

@@ -12,7 +12,8 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                                 cudaStream_t st);
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
-                             long long out_rows, double* y, int nrhs, cudaStream_t st);
+                             long long out_rows, double* y, int nrhs, double* work,
+                             long long work_doubles, cudaStream_t st);
 cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_parent,
                              const double* factors, const double* x_parent, long long parent_rows,
                              double* x_out, long long out_rows, double* y, int nrhs,
@@ -95,14 +96,16 @@ extern "C" int tf_subtree_factor(const tf_level_view* views, int32_t nlev,
 extern "C" int tf_level_solve_fwd(const tf_level_view* lv, const tf_level_view* child,
                                   const double* factors, const double* w_child,
                                   int64_t child_rows, double* w_out, int64_t out_rows, double* y,
-                                  int32_t nrhs, void* stream) {
+                                  int32_t nrhs, void* workspace, int64_t workspace_bytes,
+                                  void* stream) {
   if (!lv || nrhs < 1 || out_rows < lv->max_m) return TF_ERR_INVALID;
   if (lv->n_fronts == 0) return TF_OK;
   if (!lv->is_leaf && (!child || !w_child)) return TF_ERR_INVALID;
   LevelArgs L = make_args(lv);
   LevelArgs C = child ? make_args(child) : L;
+  if (workspace_bytes < 8 * solve_workspace_doubles(L, nrhs)) return TF_ERR_INVALID;
   return status(launch_solve_fwd(L, C, factors, w_child, child_rows, w_out, out_rows, y, nrhs,
-                                 (cudaStream_t)stream));
+                                 (double*)workspace, workspace_bytes / 8, (cudaStream_t)stream));
 }
 
 extern "C" int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,

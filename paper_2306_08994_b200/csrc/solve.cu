@@ -206,88 +206,226 @@ __global__ void __launch_bounds__(G* GPC)
 }
 
 // ------------------------------------------------------------- large fronts
-__global__ void solve_gather_fwd(LevelArgs L, LevelArgs C, const double* __restrict__ w_child,
-                                 long long child_rows, int child_at0, double* W,
-                                 long long out_rows, const double* __restrict__ y, int nrhs) {
-  const long long f = blockIdx.x;
-  const Shape s = front_shape(L, f);
-  const long long piv = L.piv_off[f];
-  const int nW = s.m * nrhs, nK = s.k * nrhs;
-  int kc[2] = {0, 0};
-  for (int c = 0; c < s.nsrc; c++)  // update rows of a small child's block start at 0
-    kc[c] = child_at0 ? 0
-                      : C.pat[(size_t)C.pattern_of[2 * (L.front_base + f) + c - C.front_base] *
-                                  TF_PAT_WIDTH + TF_PAT_K];
-  double* Wf = W + f * out_rows * nrhs;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < nW; e += gridDim.y * blockDim.x) {
-    const int r = e / nrhs, j = e - r * nrhs;
-    double v = e < nK ? y[piv * nrhs + e] : 0.0;
-    for (int c = 0; c < s.nsrc; c++) {
-      const int i = L.maps[s.ioff + c * s.m + r];
-      if (i >= 0) v += w_child[(2 * (L.front_base + f) + c - C.front_base) * child_rows * nrhs + (long long)(kc[c] + i) * nrhs + j];
-    }
-    Wf[e] = v;
+// Wavefront sweeps: one persistent launch per level and direction.  Work is
+// cut into 64x64 tiles of the fronts' panels; the tiles of the level are
+// dealt round-robin, in dependency order, to a co-resident grid, and a tile
+// waits on flags published by the tiles it depends on (acquire/release;
+// flags cleared before the launch).  Every tile's panel block (and M block)
+// is copied to shared memory asynchronously before the tile waits, so the
+// per-front dependency chain is one 64x64 product from shared memory per
+// pivot block.  Summation orders are fixed: results do not depend on timing.
+//   forward : tile (f, R) = rows [64R, 64R+64): W = gather(y, children);
+//             W -= L[R, b] Y_b for b < R in order; if R is a pivot block:
+//             Y_R = M_R W, y = Y_R / d, publish Y_R.
+//   backward: for b = nb-1 .. 0: partial tiles (f, R, b), R >= b+2:
+//             P = L[R, b]^T X_R (publish); diagonal tile (f, b):
+//             z = y_b - (L[b+1, b]^T X_{b+1} + sum_R P_R), X_b = M_b^T z.
+constexpr int TB = 64;         // tile rows = pivot block width (= factorization NB)
+constexpr int TLD = TB + 4;    // shared tile row stride (conflict-free 4-thread dots)
+constexpr int kWaveCols = 32;  // RHS columns per launch
+constexpr int kWaveFewFronts = 64;  // at most this many fronts: prefetch-heavy tile buffers
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wave_wait(const int* flag) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(flag) == 0) __nanosleep(20);
+  __syncthreads();
+}
+__device__ __forceinline__ void wave_publish(int* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
   }
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+// T[i][c] = src[i * ld + c] for i < rows, c < cols (async 16-byte copies; src
+// and T rows 16-byte aligned).  Entries outside are left as they are: the tile
+// products below bound their sums and callers ignore out-of-range outputs.
+__device__ __forceinline__ void tile_fetch(double* T, const double* src, long long ld, int rows,
+                                           int cols) {
+  const int cpr = (cols + 1) >> 1;  // 16-byte chunks per row
+  for (int e = threadIdx.x; e < rows * cpr; e += 256) {
+    const int i = e / cpr, c = (e - i * cpr) * 2;
+    if (c + 1 < cols) cp_async16(T + i * TLD + c, src + i * ld + c, true);
+    else cp_async8(T + i * TLD + c, src + i * ld + c, true);
+  }
+  cp_async_commit();
+}
 
-// Block j0: Y_b = M W_b (rows [j0, j0+kb)), y_b = Y_b / d; rows below: W_r -= L_r,b Y_b.
-__global__ void __launch_bounds__(256) solve_fwd_block(LevelArgs L, const double* __restrict__ factors,
-                                                        double* W, long long out_rows, double* y,
-                                                        int nrhs, int j0) {
-  extern __shared__ __align__(16) double sm[];
-  double* Wb = sm;                 // [SB][nrhs] right-hand block
-  double* Yb = sm + SB * nrhs;     // [SB][nrhs] solved block
-  double* Ms = Yb + SB * nrhs;     // [SB][SB] diagonal-block inverse
-  const long long f = blockIdx.x;
-  const Shape s = front_shape(L, f);
-  const int kb = min(j0 + SB, s.k) - j0;
-  if (kb <= 0) return;
-  const int j1 = j0 + kb;
-  const int r0 = j1 + blockIdx.y * RB;
-  if (blockIdx.y > 0 && r0 >= s.m) return;
-  const double* Lp = factors + f * L.fac_stride;
-  const double* M = L.aux + f * L.aux_stride + (long long)(j0 / SB) * SB * SB;
-  double* Wf = W + f * out_rows * nrhs;
-  const int n = kb * nrhs;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) Wb[e] = Wf[(long long)j0 * nrhs + e];
-#pragma unroll 4
-  for (int e = threadIdx.x; e < SB * SB; e += blockDim.x) Ms[e] = __ldg(M + e);
-  __syncthreads();
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const int r = e / nrhs, j = e - r * nrhs;
-    const double* mr = Ms + r * SB;
-    double acc = Wb[e];  // M has a unit diagonal
-    for (int q = 0; q < r; q++) acc += mr[q] * Wb[q * nrhs + j];
-    Yb[e] = acc;
-  }
-  __syncthreads();
-  if (blockIdx.y == 0) {
-    const double* dv = Lp + (long long)s.m * s.kp + j0;
-    const long long piv = L.piv_off[f] + j0;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) y[piv * nrhs + e] = Yb[e] / dv[e / nrhs];
-  }
-  const int rows = min(RB, s.m - r0);
-  if (nrhs == 1) {
-    // warp per row, lanes across the 64 block columns: coalesced panel reads
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int rl = warp; rl < rows; rl += 8) {
-      const double* lrow = Lp + (long long)(r0 + rl) * s.kp + j0;
-      double acc = 0.0;
-      if (lane < kb) acc = lrow[lane] * Yb[lane];
-      if (lane + 32 < kb) acc += lrow[lane + 32] * Yb[lane + 32];
+// out[i] = sum_{c < nc} T[i][c] v[c] (TRANS: T[c][i]); MASK -1: only c < i,
+// +1: only c > i.  One column; four threads per output, interleaved columns
+// (conflict-free with TLD = 68); the result is valid in all four threads.
+template <bool TRANS, int MASK>
+__device__ __forceinline__ double tile_dot(const double* T, const double* v, int nc) {
+  const int i = threadIdx.x >> 2, p = threadIdx.x & 3;
+  double s = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) Wf[r0 + rl] -= acc;
-    }
-    return;
+  for (int q = 0; q < 16; q++) {
+    const int c = 4 * q + p;
+    const bool on = c < nc && (MASK == 0 || (MASK < 0 ? c < i : c > i));
+    if (on) s += (TRANS ? T[c * TLD + i] : T[i * TLD + c]) * v[c];
   }
-  for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) {
-    const int rl = e / nrhs, j = e - rl * nrhs;
-    const long long r = r0 + rl;
-    const double* lrow = Lp + r * s.kp + j0;
-    double acc = Wf[r * nrhs + j];
-    for (int q = 0; q < kb; q++) acc -= lrow[q] * Yb[q * nrhs + j];
-    Wf[r * nrhs + j] = acc;
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  return s;
+}
+// General column count: entry (i, j) of the same product, v row stride nr.
+template <bool TRANS, int MASK>
+__device__ __forceinline__ double tile_dot_col(const double* T, const double* v, int i, int j,
+                                               int nr, int nc) {
+  double s = 0.0;
+  for (int c = 0; c < nc; c++) {
+    const bool on = MASK == 0 || (MASK < 0 ? c < i : c > i);
+    if (on) s += (TRANS ? T[c * TLD + i] : T[i * TLD + c]) * v[c * nr + j];
+  }
+  return s;
+}
+
+template <bool ONE>
+__global__ void __launch_bounds__(256)
+    solve_fwd_wave(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
+                   const double* __restrict__ w_child, long long child_rows, double* w_out,
+                   long long out_rows, double* y, int nr, int ldr, int col0, int* flags,
+                   double* yblk, int nb_max, int rt_max, int nbuf) {
+  // nbuf = 3: double-buffered panel tiles plus an early-fetched M tile (levels
+  // with few fronts: the per-front chain is the critical path); nbuf = 1: one
+  // tile buffer, more CTAs per SM (many fronts: throughput)
+  extern __shared__ __align__(16) double wsm[];
+  double* T0 = wsm;
+  double* T1 = nbuf >= 2 ? T0 + TB * TLD : T0;
+  double* Mt = T0 + (nbuf - 1) * TB * TLD;
+  double* Wt = T0 + nbuf * TB * TLD;  // [TB][nr]
+  double* Yb = Wt + TB * nr;          // [TB][nr]
+  const int tid = threadIdx.x;
+  const long long nf = L.n_fronts, ntiles = (long long)rt_max * nf;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int R = (int)(tile / nf);
+    const long long f = tile - (long long)R * nf;
+    const Shape s = front_shape(L, f);
+    const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+    const int r0 = R * TB;
+    if (r0 >= m) continue;
+    const int rows = min(TB, m - r0);
+    const long long piv = L.piv_off[f];
+    const double* Pf = factors + f * L.fac_stride;
+    int* fl = flags + f * nb_max;
+    double* yb = yblk + f * nb_max * TB * nr;
+    const int bend = min(R, nb);
+    // prefetch: first panel block and (pivot tiles) the M block
+    if (bend > 0) tile_fetch(T0, Pf + (long long)r0 * kp, kp, rows, min(TB, k));
+    if (R < nb && nbuf == 3) {
+      const int kbR = min(TB, k - r0);
+      tile_fetch(Mt, L.aux + f * L.aux_stride + (long long)R * TB * TB, TB, kbR, kbR);
+    }
+    // 1. the tile's rows: pivot-order RHS plus the children's update rows
+    {
+      long long chs[2] = {0, 0};
+      int kc[2] = {0, 0};
+      for (int c = 0; c < s.nsrc; c++) {
+        chs[c] = 2 * (L.front_base + f) + c - C.front_base;
+        kc[c] = child_at0 ? 0 : C.pat[(size_t)C.pattern_of[chs[c]] * TF_PAT_WIDTH + TF_PAT_K];
+      }
+      const int* inv = L.maps + s.ioff;
+      for (int e = tid; e < TB * nr; e += 256) {
+        const int rl = ONE ? e : e / nr, j = ONE ? 0 : e - rl * nr, r = r0 + rl;
+        double v = 0.0;
+        if (rl < rows) {
+          if (r < k) v = y[(piv + r) * ldr + col0 + j];
+          for (int c = 0; c < s.nsrc; c++) {
+            const int i = inv[c * m + r];
+            if (i >= 0) v += w_child[(chs[c] * child_rows + kc[c] + i) * ldr + col0 + j];
+          }
+        }
+        Wt[e] = v;
+      }
+    }
+    // 2. earlier pivot blocks, in order (next block's tile in flight)
+    for (int b = 0; b < bend; b++) {
+      double* T = (b & 1) ? T1 : T0;
+      if (nbuf >= 2 && b + 1 < bend) {
+        tile_fetch((b & 1) ? T0 : T1, Pf + (long long)r0 * kp + (b + 1) * TB, kp, rows,
+                   min(TB, k - (b + 1) * TB));
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      wave_wait(fl + b);
+      const int kb = min(TB, k - b * TB);
+      for (int e = tid; e < TB * nr; e += 256) Yb[e] = e < kb * nr ? __ldcg(yb + (long long)b * TB * nr + e) : 0.0;
+      __syncthreads();
+      if (ONE) {
+        const double sdot = tile_dot<false, 0>(T, Yb, kb);
+        if ((tid & 3) == 0 && (tid >> 2) < rows) Wt[tid >> 2] -= sdot;
+      } else {
+        for (int e = tid; e < rows * nr; e += 256) {
+          const int i = e / nr, j = e - i * nr;
+          Wt[e] -= tile_dot_col<false, 0>(T, Yb, i, j, nr, kb);
+        }
+      }
+      __syncthreads();
+      if (nbuf == 1 && b + 1 < bend)
+        tile_fetch(T0, Pf + (long long)r0 * kp + (b + 1) * TB, kp, rows, min(TB, k - (b + 1) * TB));
+    }
+    // 3. pivot tile: Y = M W on its pivot rows (unit diagonal); publish; own update rows
+    if (R < nb) {
+      const int kb = min(TB, k - r0);
+      if (nbuf < 3) tile_fetch(Mt, L.aux + f * L.aux_stride + (long long)R * TB * TB, TB, kb, kb);
+      cp_async_wait<0>();
+      __syncthreads();
+      if (ONE) {
+        const double sdot = tile_dot<false, -1>(Mt, Wt, kb);
+        const int i = tid >> 2;
+        if ((tid & 3) == 0) Yb[i] = i < kb ? Wt[i] + sdot : 0.0;
+      } else {
+        for (int e = tid; e < TB * nr; e += 256) {
+          const int i = e / nr, j = e - i * nr;
+          Yb[e] = i < kb ? Wt[e] + tile_dot_col<false, -1>(Mt, Wt, i, j, nr, kb) : 0.0;
+        }
+      }
+      __syncthreads();
+      const double* dv = Pf + (long long)m * kp + r0;
+      for (int e = tid; e < kb * nr; e += 256) {
+        const int c = ONE ? e : e / nr, j = ONE ? 0 : e - c * nr;
+        yb[(long long)R * TB * nr + e] = Yb[e];
+        y[(piv + r0 + c) * ldr + col0 + j] = Yb[e] / dv[c];
+      }
+      wave_publish(fl + R);
+      if (rows > kb) {  // update rows inside the pivot tile: W -= L[rows, own block] Y
+        tile_fetch(T0, Pf + (long long)r0 * kp + r0, kp, rows, kb);
+        cp_async_wait<0>();
+        __syncthreads();
+        if (ONE) {
+          const double sdot = tile_dot<false, 0>(T0, Yb, kb);
+          const int i = tid >> 2;
+          if ((tid & 3) == 0 && i >= kb && i < rows) Wt[i] -= sdot;
+        } else {
+          for (int e = tid; e < rows * nr; e += 256) {
+            const int i = e / nr, j = e - i * nr;
+            if (i >= kb) Wt[e] -= tile_dot_col<false, 0>(T0, Yb, i, j, nr, kb);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // 4. the tile's update rows, in place
+    for (int e = tid; e < rows * nr; e += 256) {
+      const int rl = ONE ? e : e / nr, j = ONE ? 0 : e - rl * nr, r = r0 + rl;
+      if (r >= k) w_out[(f * out_rows + r) * ldr + col0 + j] = Wt[e];
+    }
+    __syncthreads();
   }
 }
 
@@ -318,83 +456,152 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
   }
 }
 
-// partial[f][x][c][j] = sum_{r in chunk x of [j1, m)} L[r][j0+c] X[r][j]
-__global__ void __launch_bounds__(256) solve_bwd_partial(LevelArgs L, const double* __restrict__ factors,
-                                                          const double* __restrict__ X,
-                                                          long long out_rows, int nrhs, int j0,
-                                                          double* partial, int nchunk) {
-  extern __shared__ __align__(16) double sm[];  // Xr [RB][nrhs]
-  const long long f = blockIdx.x;
-  const Shape s = front_shape(L, f);
-  const int kb = min(j0 + SB, s.k) - j0;
-  if (kb <= 0) return;
-  const int j1 = j0 + kb;
-  const int r0 = j1 + blockIdx.y * RB;
-  double* P = partial + ((f * nchunk + blockIdx.y) * SB) * (long long)nrhs;
-  const int n = kb * nrhs;
-  if (r0 >= s.m) {
-    for (int e = threadIdx.x; e < n; e += blockDim.x) P[e] = 0.0;
-    return;
-  }
-  const double* Lp = factors + f * L.fac_stride;
-  const double* Xf = X + f * out_rows * nrhs;
-  const int rows = min(RB, s.m - r0);
-  for (int e = threadIdx.x; e < rows * nrhs; e += blockDim.x) sm[e] = Xf[(long long)r0 * nrhs + e];
-  __syncthreads();
-  if (nrhs == 1) {
-    // 64 columns x 4 row groups, fixed-order reduction of the 4 partial sums
-    __shared__ double red[4][SB];
-    const int c = threadIdx.x & (SB - 1), g = threadIdx.x >> 6;
-    double acc = 0.0;
-    if (c < kb) {
-      const double* lcol = Lp + (long long)r0 * s.kp + j0 + c;
-      for (int q = g; q < rows; q += 4) acc += lcol[(long long)q * s.kp] * sm[q];
-    }
-    red[g][c] = acc;
-    __syncthreads();
-    if (g == 0 && c < kb) P[c] = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
-    return;
-  }
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const int j = e / kb, c = e - j * kb;  // c fastest: coalesced panel reads
-    const double* lcol = Lp + (long long)r0 * s.kp + j0 + c;
-    double acc = 0.0;
-    for (int q = 0; q < rows; q++) acc += lcol[(long long)q * s.kp] * sm[q * nrhs + j];
-    P[c * nrhs + j] = acc;
+// Load rows [r0, r0 + rows) of a front's x block (columns col0..col0+nr) into Xs
+// [TB][nr], zero-padded; produced rows are read through L2 (__ldcg).
+__device__ __forceinline__ void load_x_rows(double* Xs, const double* Xf, int r0, int rows,
+                                            int nr, int ldr) {
+  for (int e = threadIdx.x; e < TB * nr; e += 256) {
+    const int i = e / nr, j = e - i * nr;
+    Xs[e] = i < rows ? __ldcg(Xf + (long long)(r0 + i) * ldr + j) : 0.0;
   }
 }
 
-// X_b = M^T (X_b - sum_x partial[x]); writes X rows [j0, j0+kb) and y.
-__global__ void __launch_bounds__(256) solve_bwd_block(LevelArgs L, double* X, long long out_rows,
-                                                        double* y, int nrhs, int j0,
-                                                        const double* __restrict__ partial,
-                                                        int nchunk) {
-  extern __shared__ __align__(16) double sm[];  // Rb [SB][nrhs], then M [SB][SB]
-  const long long f = blockIdx.x;
-  const Shape s = front_shape(L, f);
-  const int kb = min(j0 + SB, s.k) - j0;
-  if (kb <= 0) return;
-  const int j1 = j0 + kb;
-  const int used = s.m > j1 ? (s.m - j1 + RB - 1) / RB : 0;
-  const double* M = L.aux + f * L.aux_stride + (long long)(j0 / SB) * SB * SB;
-  double* Xf = X + f * out_rows * nrhs;
-  const int n = kb * nrhs;
-  double* Ms = sm + SB * nrhs;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < SB * SB; e += blockDim.x) Ms[e] = __ldg(M + e);
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    double v = Xf[(long long)j0 * nrhs + e];
-    for (int x = 0; x < used; x++) v -= partial[((f * nchunk + x) * SB) * (long long)nrhs + e];
-    sm[e] = v;
-  }
-  __syncthreads();
-  const long long piv = L.piv_off[f] + j0;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const int c = e / nrhs, j = e - c * nrhs;
-    double acc = sm[e];  // (M^T)[c][c] = 1
-    for (int q = c + 1; q < kb; q++) acc += Ms[q * SB + c] * sm[q * nrhs + j];
-    Xf[(long long)j0 * nrhs + e] = acc;
-    y[piv * nrhs + e] = acc;
+template <bool ONE>
+__global__ void __launch_bounds__(256)
+    solve_bwd_wave(LevelArgs L, const double* __restrict__ factors, double* X, long long out_rows,
+                   double* y, int nr, int ldr, int col0, int* flags, double* part, int nb_max,
+                   int rt_max, int nbuf) {
+  extern __shared__ __align__(16) double wsm[];
+  double* T = wsm;                             // panel tile
+  double* Mt = T + (nbuf - 1) * TB * TLD;      // M tile (aliases T when nbuf == 1)
+  double* Xs = T + nbuf * TB * TLD;            // [TB][nr]
+  double* Z = Xs + TB * nr;        // [TB][nr]
+  const int tid = threadIdx.x;
+  const long long nf = L.n_fronts;
+  int* flx = flags;                                  // [nf][nb_max]: X_b final
+  int* flp = flags + nf * nb_max;                    // [nf][rt_max][nb_max]: partial (R, b)
+  // dependency order: for b = nb_max-1 .. 0: partial tiles (f, R >= b+2), then pivot tiles (f, b)
+  long long next = blockIdx.x, base = 0;
+  for (int b = nb_max - 1; b >= 0; b--) {
+    const long long npart = nf * (long long)max(0, rt_max - b - 2), count = npart + nf;
+    for (; next < base + count; next += gridDim.x) {
+      const long long item = next - base;
+      const bool partial = item < npart;
+      const long long f = partial ? item % nf : item - npart;
+      const int R = partial ? b + 2 + (int)(item / nf) : b + 1;
+      const Shape s = front_shape(L, f);
+      const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+      const int rt = (m + TB - 1) / TB;
+      if (b >= nb || (partial && R >= rt)) continue;
+      const int j0 = b * TB, kb = min(TB, k - j0);
+      const long long piv = L.piv_off[f];
+      const double* Pf = factors + f * L.fac_stride;
+      double* Xf = X + f * out_rows * ldr + col0;
+      if (partial) {
+        // P = L[R, b]^T X_R
+        double* pp = part + ((f * rt_max + R) * (long long)nb_max + b) * TB * nr;
+        const int r0 = R * TB, rows = min(TB, m - r0);
+        tile_fetch(T, Pf + (long long)r0 * kp + j0, kp, rows, kb);
+        if (R < nb) wave_wait(flx + f * nb_max + R);
+        load_x_rows(Xs, Xf, r0, rows, nr, ldr);
+        cp_async_wait<0>();
+        __syncthreads();
+        if (ONE) {
+          const double sdot = tile_dot<true, 0>(T, Xs, rows);
+          if ((tid & 3) == 0) pp[tid >> 2] = sdot;
+        } else {
+          for (int e = tid; e < kb * nr; e += 256) {
+            const int c = e / nr, j = e - c * nr;
+            pp[e] = tile_dot_col<true, 0>(T, Xs, c, j, nr, rows);
+          }
+        }
+        wave_publish(flp + (f * rt_max + R) * (long long)nb_max + b);
+        __syncthreads();
+        continue;
+      }
+      // pivot tile b.  z = y_b - sum over rows r >= j0 + kb of L[r, b]^T x_r:
+      //   (a) update rows sharing the block's own row tile (last block, kb < 64),
+      //   (b) partial tiles R >= b+2 (published earlier), in order,
+      //   (c) row tile b+1 (waits for X_{b+1}): the dependency chain.
+      if (nbuf == 2) tile_fetch(Mt, L.aux + f * L.aux_stride + (long long)b * TB * TB, TB, kb, kb);
+      for (int e = tid; e < TB * nr; e += 256) Z[e] = 0.0;
+      if (kb < TB && j0 + kb < m) {
+        const int rows = min(TB, m - j0);
+        tile_fetch(T, Pf + (long long)j0 * kp + j0, kp, rows, kb);
+        for (int e = tid; e < TB * nr; e += 256) {
+          const int i = e / nr, j = e - i * nr;
+          Xs[e] = (i >= kb && i < rows) ? __ldcg(Xf + (long long)(j0 + i) * ldr + j) : 0.0;
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        if (ONE) {
+          const double sdot = tile_dot<true, 0>(T, Xs, rows);
+          if ((tid & 3) == 0) Z[tid >> 2] = sdot;
+        } else {
+          for (int e = tid; e < kb * nr; e += 256) {
+            const int c = e / nr, j = e - c * nr;
+            Z[e] = tile_dot_col<true, 0>(T, Xs, c, j, nr, rows);
+          }
+        }
+        __syncthreads();
+      }
+      const int R1 = b + 1, rows1 = R1 < rt ? min(TB, m - R1 * TB) : 0;
+      if (rows1 > 0) tile_fetch(T, Pf + (long long)R1 * TB * kp + j0, kp, rows1, kb);
+      // (b): every partial's flag polled by its own thread, summed in order
+      for (int Rq = b + 2 + tid; Rq < rt; Rq += 256)
+        while (ld_acquire(flp + (f * rt_max + Rq) * (long long)nb_max + b) == 0) __nanosleep(20);
+      __syncthreads();
+      for (int e = tid; e < kb * nr; e += 256) {
+        double acc = Z[e];
+        for (int Rq = b + 2; Rq < rt; Rq++)
+          acc += __ldcg(part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB * nr + e);
+        Z[e] = acc;
+      }
+      // (c)
+      if (rows1 > 0 && R1 < nb) wave_wait(flx + f * nb_max + R1);
+      load_x_rows(Xs, Xf, R1 * TB, rows1, nr, ldr);
+      cp_async_wait<0>();
+      __syncthreads();
+      if (rows1 > 0) {
+        if (ONE) {
+          const double sdot = tile_dot<true, 0>(T, Xs, rows1);
+          if ((tid & 3) == 0) Z[tid >> 2] += sdot;
+        } else {
+          for (int e = tid; e < kb * nr; e += 256) {
+            const int c = e / nr, j = e - c * nr;
+            Z[e] += tile_dot_col<true, 0>(T, Xs, c, j, nr, rows1);
+          }
+        }
+      }
+      __syncthreads();
+      if (nbuf == 1) tile_fetch(Mt, L.aux + f * L.aux_stride + (long long)b * TB * TB, TB, kb, kb);
+      for (int e = tid; e < TB * nr; e += 256) {
+        const int c = e / nr, j = e - c * nr;
+        Z[e] = c < kb ? y[(piv + j0 + c) * ldr + col0 + j] - Z[e] : 0.0;
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      // X_b = M^T z (M: strict lower part, unit diagonal)
+      if (ONE) {
+        const double sdot = tile_dot<true, 1>(Mt, Z, kb);
+        const int c = tid >> 2;
+        if ((tid & 3) == 0 && c < kb) {
+          const double xv = Z[c] + sdot;
+          Xf[(long long)(j0 + c) * ldr] = xv;
+          y[(piv + j0 + c) * ldr + col0] = xv;
+        }
+      } else {
+        for (int e = tid; e < kb * nr; e += 256) {
+          const int c = e / nr, j = e - c * nr;
+          const double xv = Z[e] + tile_dot_col<true, 1>(Mt, Z, c, j, nr, kb);
+          Xf[(long long)(j0 + c) * ldr + j] = xv;
+          y[(piv + j0 + c) * ldr + col0 + j] = xv;
+        }
+      }
+      wave_publish(flx + f * nb_max + b);
+      __syncthreads();
+    }
+    base += count;
   }
 }
 
@@ -491,32 +698,68 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
   return cudaSuccess;
 }
 
+// Large levels: Y blocks (forward) or partial products (backward), then flags.
+static long long wave_blocks_doubles(const LevelArgs& L, int nrhs) {
+  const long long nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
+  return (long long)L.n_fronts * rt * nb * TB * std::min(nrhs, kWaveCols);
+}
 long long solve_workspace_doubles(const LevelArgs& L, int nrhs) {
   if (!level_is_large(L.is_leaf, L.max_m)) return 0;
-  const long long nchunk = (L.max_m + RB - 1) / RB;
-  return (long long)L.n_fronts * nchunk * SB * nrhs;
+  const long long nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
+  return wave_blocks_doubles(L, nrhs) + ((long long)L.n_fronts * nb * (1 + rt) + 1) / 2 + 1;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 1;
+  }
+  return n;
+}
+
+// Co-resident grid for a persistent wavefront kernel (tiles wait on each other).
+template <class K>
+static unsigned wave_grid(K kern, size_t smem, long long ntiles) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  const long long cap = (long long)num_sms() * std::max(occ, 1);
+  return (unsigned)std::max(1LL, std::min(ntiles, cap));
 }
 
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
-                             long long out_rows, double* y, int nrhs, cudaStream_t st) {
+                             long long out_rows, double* y, int nrhs, double* work,
+                             long long work_doubles, cudaStream_t st) {
+  const int child_at0 = level_is_large(C.is_leaf, C.max_m) ? 0 : 1;
   if (!level_is_large(L.is_leaf, L.max_m))
-    return dispatch_small<true>(L, C, level_is_large(C.is_leaf, C.max_m) ? 0 : 1, factors, w_child,
-                                child_rows, w_out, out_rows, y, nrhs, st);
-  const unsigned nf = (unsigned)L.n_fronts;
-  const long long nW = (long long)L.max_m * nrhs;
-  timer_begin(K_SOLVE_GATHER, st);
-  solve_gather_fwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
-                     st>>>(L, C, w_child, child_rows, level_is_large(C.is_leaf, C.max_m) ? 0 : 1, w_out, out_rows, y,
-                          nrhs);
-  timer_end(st);
-  const size_t smem = sizeof(double) * (2 * SB * (size_t)nrhs + SB * SB);
-  cudaFuncSetAttribute(solve_fwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int j0 = 0; j0 < L.max_k; j0 += SB) {
-    const int rows = std::max(1, L.max_m - j0 - 1);
+    return dispatch_small<true>(L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, y,
+                                nrhs, st);
+  if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
+  const int nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
+  const int cw = std::min(nrhs, kWaveCols);
+  double* yblk = work;
+  int* flags = reinterpret_cast<int*>(work + wave_blocks_doubles(L, nrhs));
+  for (int col0 = 0; col0 < nrhs; col0 += cw) {
+    const int nr = std::min(cw, nrhs - col0);
+    const int nbuf = L.n_fronts <= kWaveFewFronts ? 3 : 1;
+    const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
+    if (nb > 0) cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb, st);
     timer_begin(K_SOLVE_FWD_BLOCK, st);
-    solve_fwd_block<<<dim3(nf, (unsigned)((rows + RB - 1) / RB)), 256, smem, st>>>(
-        L, factors, w_out, out_rows, y, nrhs, j0);
+    if (nr == 1) {
+      const unsigned g = wave_grid(solve_fwd_wave<true>, smem, (long long)rt * L.n_fronts);
+      solve_fwd_wave<true><<<g, 256, smem, st>>>(L, C, child_at0, factors, w_child, child_rows,
+                                                  w_out, out_rows, y, nr, nrhs, col0, flags, yblk,
+                                                  nb, rt, nbuf);
+    } else {
+      const unsigned g = wave_grid(solve_fwd_wave<false>, smem, (long long)rt * L.n_fronts);
+      solve_fwd_wave<false><<<g, 256, smem, st>>>(L, C, child_at0, factors, w_child, child_rows,
+                                                   w_out, out_rows, y, nr, nrhs, col0, flags,
+                                                   yblk, nb, rt, nbuf);
+    }
     timer_end(st);
   }
   return cudaGetLastError();
@@ -536,22 +779,28 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   solve_gather_bwd<<<dim3(nf, (unsigned)std::min<long long>((nW + 255) / 256, 1024)), 256, 0,
                      st>>>(L, PA, has_parent, x_parent, parent_rows, x_out, out_rows, y, nrhs);
   timer_end(st);
-  const int nchunk = (L.max_m + RB - 1) / RB;
-  const size_t smp = sizeof(double) * RB * (size_t)nrhs;
-  const size_t smb = sizeof(double) * (SB * (size_t)nrhs + SB * SB);
-  cudaFuncSetAttribute(solve_bwd_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
-  cudaFuncSetAttribute(solve_bwd_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
-  const int nblk = (L.max_k + SB - 1) / SB;
-  for (int b = nblk - 1; b >= 0; b--) {
-    const int j0 = b * SB;
-    const int rows = std::max(1, L.max_m - j0 - 1);
-    const int used = (rows + RB - 1) / RB;
-    timer_begin(K_SOLVE_BWD_PARTIAL, st);
-    solve_bwd_partial<<<dim3(nf, (unsigned)used), 256, smp, st>>>(L, factors, x_out, out_rows,
-                                                                  nrhs, j0, work, nchunk);
-    timer_end(st);
+  const int nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
+  if (nb == 0) return cudaGetLastError();
+  const int cw = std::min(nrhs, kWaveCols);
+  double* part = work;
+  int* flags = reinterpret_cast<int*>(work + wave_blocks_doubles(L, nrhs));
+  long long ntiles = 0;
+  for (int b = 0; b < nb; b++) ntiles += (long long)L.n_fronts * (std::max(0, rt - b - 2) + 1);
+  for (int col0 = 0; col0 < nrhs; col0 += cw) {
+    const int nr = std::min(cw, nrhs - col0);
+    const int nbuf = L.n_fronts <= kWaveFewFronts ? 2 : 1;
+    const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
+    cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb * (1 + rt), st);
     timer_begin(K_SOLVE_BWD_BLOCK, st);
-    solve_bwd_block<<<nf, 256, smb, st>>>(L, x_out, out_rows, y, nrhs, j0, work, nchunk);
+    if (nr == 1) {
+      const unsigned g = wave_grid(solve_bwd_wave<true>, smem, ntiles);
+      solve_bwd_wave<true><<<g, 256, smem, st>>>(L, factors, x_out, out_rows, y, nr, nrhs, col0,
+                                                  flags, part, nb, rt, nbuf);
+    } else {
+      const unsigned g = wave_grid(solve_bwd_wave<false>, smem, ntiles);
+      solve_bwd_wave<false><<<g, 256, smem, st>>>(L, factors, x_out, out_rows, y, nr, nrhs, col0,
+                                                   flags, part, nb, rt, nbuf);
+    }
     timer_end(st);
   }
   return cudaGetLastError();
@@ -559,8 +808,9 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   if (!level_is_large(L.is_leaf, L.max_m)) return (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
-  const int nblk = (L.max_k + SB - 1) / SB;
-  return fwd ? 1 + nblk : 1 + 2 * nblk;
+  const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
+  if (fwd) return slices;
+  return 1 + (L.max_k > 0 ? slices : 0);
 }
 
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,

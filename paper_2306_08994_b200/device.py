@@ -235,7 +235,7 @@ class DevicePlan:
                                         C.byref(child.view) if child else None,
                                         _ptr(self.factors[L]), _ptr(prev),
                                         child.max_m if child else 0, _ptr(cur), dl.max_m,
-                                        _ptr(y), nrhs, sp)
+                                        _ptr(y), nrhs, _ptr(self._ws), self._ws_bytes, sp)
             _lib.check(rc, f"tf_level_solve_fwd(level {L})")
             prev = cur
         prev = None

@@ -384,7 +384,8 @@ class ShardedFactorization:
                     C.c_void_p(self._blk[r][(L - 1) & 1].data_ptr()) if L > 0 else None,
                     dp.levels[L - 1].max_m if L > 0 else 0,
                     C.c_void_p(self._blk[r][L & 1].data_ptr() + 8 * (f0 - lo) * rows),
-                    dp.levels[L].max_m, C.c_void_p(self._y[r].data_ptr()), nrhs, sp)
+                    dp.levels[L].max_m, C.c_void_p(self._y[r].data_ptr()), nrhs,
+                    C.c_void_p(self._ws[r][0].data_ptr()), self._ws[r][1], sp)
                 _lib.check(rc, f"tf_level_solve_fwd(rank {r}, level {L})")
         for L in range(nl - 1, -1, -1):
             if L + 1 < nl:

@@ -101,7 +101,7 @@ def solve_levels(nrhs):
         ch = dp.levels[L - 1] if L > 0 else None
         assert lib.tf_level_solve_fwd(C.byref(dl.view), C.byref(ch.view) if ch else None,
                                       P(dp.factors[L]), P(prev), ch.max_m if ch else 0, P(cur),
-                                      dl.max_m, P(y), nrhs, sp) == 0
+                                      dl.max_m, P(y), nrhs, P(dp._ws), dp._ws_bytes, sp) == 0
         prev = cur
         evf[L + 1].record()
     prev = None
