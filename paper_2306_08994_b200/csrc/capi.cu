@@ -25,7 +25,7 @@ int subtree_fusable_levels(const LevelArgs* lv, int n_levels);
 cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* fac,
                                   const double* elem, double* upd_out, double thr,
                                   unsigned long long* err, cudaStream_t st);
-int large_panel_launches(int max_k, int n_fronts);
+int large_level_launches(int max_k, int max_upd, long long level_fronts);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
 int g_small_max_m = 112;  // measured best split on B200 (tools/sweep.sh)
 }  // namespace tfb
@@ -135,8 +135,7 @@ extern "C" int32_t tf_level_launch_count(const tf_level_view* lv, int32_t nrhs, 
   LevelArgs L = make_args(lv);
   if (phase == 0) {
     if (!level_is_large(lv->is_leaf, lv->max_m)) return 1;
-    return 1 + large_panel_launches(lv->max_k, (int)L.level_fronts) + (lv->max_k > 0 && lv->max_upd > 0 ? 1 : 0) +
-           (lv->max_k > 0 ? 1 : 0);
+    return large_level_launches(lv->max_k, lv->max_upd, L.level_fronts);
   }
   return solve_launches(L, nrhs, phase == 1);
 }

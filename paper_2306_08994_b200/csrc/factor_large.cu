@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
     bRow0 = k + (int)tile_c0;
     nA = min(BM, u - (int)tile_r0);
     nB = min(BN, u - (int)tile_c0);
-    aK0 = bK0 = 0;
-    kLen = k;
+    aK0 = bK0 = t1 > t0 ? t0 : 0;  // pivot columns [t0, t1) (lookahead chunks) or all
+    kLen = t1 > t0 ? min(t1, k) - t0 : k;
   } else {
     const int kb = min(t0 + NB, k) - t0;
     if (kb <= 0) return;
@@ -723,11 +723,24 @@ static void gemm_attr() {
 }
 
 template <class G>
-static void launch_schur(const LevelArgs& L, double* factors, double* upd_out, cudaStream_t st) {
+static void launch_schur(const LevelArgs& L, double* factors, double* upd_out, cudaStream_t st,
+                         int t0 = 0, int t1 = 0) {
   gemm_attr<1, G>();
   dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + G::BN - 1) / G::BN),
          (unsigned)((L.max_upd + G::BM - 1) / G::BM));
-  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, 0, 0);
+  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, t0, t1);
+}
+
+// P[r][c] -= sum_{t in [t0, t1)} l_rt d_t l_ct for c in [c0, c1), r >= c.
+static void launch_panel_update(const LevelArgs& L, double* factors, int c0, int c1, int t0,
+                                int t1, cudaStream_t st) {
+  dim3 g((unsigned)L.n_fronts, (unsigned)((c1 - c0 + GPanel::BN - 1) / GPanel::BN),
+         (unsigned)((L.max_m - c0 + GPanel::BM - 1) / GPanel::BM));
+  gemm_attr<0, GPanel>();
+  timer_begin(K_PANEL, st);
+  large_update_kernel<0, GPanel><<<g, GPanel::NT, GPanel::smem, st>>>(L, factors, nullptr, c0, c0,
+                                                                      c1, t0, t1);
+  timer_end(st);
 }
 
 static int gemm_variant() {
@@ -770,16 +783,85 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
   if (mid >= b) mid = a + NB;
   cudaError_t e = panel_factor(L, factors, thr, err, a, mid, st);
   if (e != cudaSuccess) return e;
-  dim3 g((unsigned)L.n_fronts, (unsigned)((b - mid + GPanel::BN - 1) / GPanel::BN),
-         (unsigned)((L.max_m - mid + GPanel::BM - 1) / GPanel::BM));
-  gemm_attr<0, GPanel>();
-  timer_begin(K_PANEL, st);
-  large_update_kernel<0, GPanel><<<g, GPanel::NT, GPanel::smem, st>>>(L, factors, nullptr, mid, mid, b,
-                                                                  a, mid);
-  timer_end(st);
+  launch_panel_update(L, factors, mid, b, a, mid, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return panel_factor(L, factors, thr, err, mid, b, st);
+}
+
+// Levels with few, wide fronts: the pivot chain (diagonal blocks, their
+// triangular solves, panel updates) is latency-bound, so the Schur update and
+// the bulk of the panel updates run concurrently with it, one super-block of
+// kLookaheadCols pivot columns at a time (right-looking, lookahead 1):
+//   chain  (high priority): factor super-block j; update super-block j+1 by j
+//   panel  (high priority): update the panel columns beyond j+1 by j
+//   schur  (low priority) : S -= L21_j D_j L21_j^T
+// Every entry is updated by the super-blocks in increasing order, as in the
+// sequential path, so results are identical run to run.
+constexpr int kLookaheadCols = 256;
+constexpr int kLookaheadMaxFronts = 128;
+
+struct LookaheadStreams {
+  cudaStream_t chain = nullptr, panel = nullptr, schur = nullptr;
+  cudaEvent_t start, chain_done, panel_done, schur_done;
+};
+static LookaheadStreams& lookahead_streams() {
+  static LookaheadStreams ls;
+  if (!ls.chain) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&ls.chain, cudaStreamNonBlocking, greatest);
+    cudaStreamCreateWithPriority(&ls.panel, cudaStreamNonBlocking, greatest);
+    cudaStreamCreateWithPriority(&ls.schur, cudaStreamNonBlocking, least);
+    for (cudaEvent_t* ev : {&ls.start, &ls.chain_done, &ls.panel_done, &ls.schur_done})
+      cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  }
+  return ls;
+}
+
+static cudaError_t factor_lookahead(const LevelArgs& L, double* factors, double* upd_out,
+                                    double thr, unsigned long long* err, cudaStream_t st) {
+  LookaheadStreams& S = lookahead_streams();
+  cudaEventRecord(S.start, st);  // after the assembly
+  cudaStreamWaitEvent(S.chain, S.start, 0);
+  cudaStreamWaitEvent(S.panel, S.start, 0);
+  cudaStreamWaitEvent(S.schur, S.start, 0);
+  const int nsb = (L.max_k + kLookaheadCols - 1) / kLookaheadCols;
+  const bool schur = L.max_upd > 0;
+  for (int j = 0; j < nsb; j++) {
+    const int c0 = j * kLookaheadCols, c1 = std::min(c0 + kLookaheadCols, L.max_k);
+    const int c2 = std::min(c1 + kLookaheadCols, L.max_k);
+    cudaError_t e = panel_factor(L, factors, thr, err, c0, c1, S.chain);
+    if (e != cudaSuccess) return e;
+    if (j + 1 < nsb) {
+      // the panel stream's update by j-1 covers columns >= c1: it must land first
+      if (j >= 1) cudaStreamWaitEvent(S.chain, S.panel_done, 0);
+      launch_panel_update(L, factors, c1, c2, c0, c1, S.chain);
+    }
+    cudaEventRecord(S.chain_done, S.chain);
+    if (j + 2 < nsb) {
+      cudaStreamWaitEvent(S.panel, S.chain_done, 0);
+      launch_panel_update(L, factors, c2, L.max_k, c0, c1, S.panel);
+      cudaEventRecord(S.panel_done, S.panel);
+    }
+    if (schur) {
+      cudaStreamWaitEvent(S.schur, S.chain_done, 0);
+      timer_begin(K_SCHUR, S.schur);
+      launch_schur<GSchurA>(L, factors, upd_out, S.schur, c0, c1);
+      timer_end(S.schur);
+    }
+  }
+  cudaEventRecord(S.chain_done, S.chain);
+  cudaEventRecord(S.panel_done, S.panel);
+  cudaEventRecord(S.schur_done, S.schur);
+  cudaStreamWaitEvent(st, S.chain_done, 0);
+  cudaStreamWaitEvent(st, S.panel_done, 0);
+  cudaStreamWaitEvent(st, S.schur_done, 0);
+  dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
+  timer_begin(K_FINALIZE, st);
+  large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
+  timer_end(st);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, double* factors,
@@ -810,6 +892,8 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (L.max_k > kLookaheadCols && L.level_fronts <= kLookaheadMaxFronts)
+    return factor_lookahead(L, factors, upd_out, thr, err, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);
     if (e != cudaSuccess) return e;
@@ -847,6 +931,22 @@ int large_panel_launches(int max_k, int n_fronts) {
   int mid = (max_k / 2 + NB - 1) / NB * NB;
   if (mid >= max_k) mid = NB;
   return large_panel_launches(mid, n_fronts) + 1 + large_panel_launches(max_k - mid, n_fronts);
+}
+
+// Kernel launches of one launch_factor_large call (tf_level_launch_count).
+int large_level_launches(int max_k, int max_upd, long long level_fronts) {
+  const int fronts = (int)std::min<long long>(level_fronts, 1 << 30);
+  if (max_k > kLookaheadCols && level_fronts <= kLookaheadMaxFronts) {
+    const int nsb = (max_k + kLookaheadCols - 1) / kLookaheadCols;
+    int n = 2;  // assembly, finalize
+    for (int j = 0; j < nsb; j++) {
+      const int c0 = j * kLookaheadCols, c1 = std::min(c0 + kLookaheadCols, max_k);
+      n += large_panel_launches(c1 - c0, fronts) + (j + 1 < nsb) + (j + 2 < nsb) + (max_upd > 0);
+    }
+    return n;
+  }
+  return 1 + large_panel_launches(max_k, fronts) + (max_k > 0 && max_upd > 0 ? 1 : 0) +
+         (max_k > 0 ? 1 : 0);
 }
 
 }  // namespace tfb
