@@ -43,6 +43,11 @@ extern "C" {
                            source 0 at maps[IOFF, IOFF+m), source 1 at [IOFF+m, IOFF+2m) */
 #define TF_PAT_KP 9     /* panel leading dimension: k rounded up to a multiple of 4 */
 #define TF_PAT_FAC 10   /* doubles of the front's factor slot: m*kp (panel) + kp (diag) */
+#define TF_PAT_SOFF 11  /* offset in the maps array of the extend-add scatter table
+                           (fronts of order <= 232; -1 otherwise): entry e of source c
+                           (packed lower order, source 1 after tri(len0) entries of
+                           source 0) -> position in the shared-memory front layout
+                           [pivot rows packed | L21 rows of stride kp+1 | Schur block packed] */
 
 /* ------------------------------------------------------------------ mesh */
 

@@ -20,7 +20,7 @@ TF_ERR_CUDA = -2
 
 PAT_WIDTH = 12
 (PAT_M, PAT_K, PAT_NSRC, PAT_LEN0, PAT_LEN1, PAT_OFF0, PAT_OFF1, PAT_LEAF, PAT_IOFF, PAT_KP,
- PAT_FAC) = range(11)
+ PAT_FAC, PAT_SOFF) = range(12)
 
 
 class PlanSummary(C.Structure):

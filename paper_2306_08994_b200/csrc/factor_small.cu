@@ -24,7 +24,21 @@
 
 namespace tfb {
 
-int small_smem_per_group(int max_m);
+// Shared-memory front layout (tri(m) + (m-k)(kp+1-k) doubles):
+//   rows r < k  : packed lower triangle, F[tri(r) + c]             (pivot block)
+//   rows r >= k : rows of odd stride ks = kp+1 (bank-conflict-free column
+//                 access), F[tri(k) + (r-k) ks + c]                (L21)
+//   Schur block : packed lower tri(m-k) at tri(k) + (m-k) ks  (the update
+//                 slot's layout: copies out contiguously)
+// The extend-add targets come from the pattern's scatter table
+// (symbolic.cpp): entry e of source c lands at F[scat[e]].
+__host__ __device__ inline int small_front_doubles(int max_m, int max_k) {
+  (void)max_k;
+  return (int)tri32(max_m, 0) + 4 * max_m + max_m;  // + pivot/column scratch
+}
+int small_smem_per_group(int max_m, int max_k) {
+  return (int)((sizeof(double) * (size_t)small_front_doubles(max_m, max_k) + 15) & ~(size_t)15);
+}
 
 // Thread t's contiguous chunk [beg, end) of n items split over G threads.
 __device__ __forceinline__ void chunk_of(int n, int G, int t, int& beg, int& end) {
@@ -40,54 +54,35 @@ template <int G>
 __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, const Shape& S,
                                              const double* __restrict__ src0,
                                              const double* __restrict__ src1, double* F,
-                                             double* lv, int* mp, double* __restrict__ fac_out,
+                                             double* lv, double* __restrict__ fac_out,
                                              double* __restrict__ upd_dst, double threshold,
                                              unsigned long long* err, int t, int bar) {
   const int m = S.m, k = S.k, kp = S.kp, u = m - k;
-  const int nF = (int)tri32(m, 0);
-
-  for (int e = t; e < nF; e += G) F[e] = 0.0;
-  for (int i = t; i < S.len0; i += G) mp[i] = L.maps[S.off0 + i];
-  for (int i = t; i < S.len1; i += G) mp[S.len0 + i] = L.maps[S.off1 + i];
+  const int ks = kp + 1, tk = (int)tri32(k, 0), nS = (int)tri32(u, 0), s0 = tk + u * ks;
+  double* Sb = F + s0;
+  auto rowp = [&](int r) { return r < k ? (int)tri32(r, 0) : tk + (r - k) * ks; };
+  for (int e = t; e < s0 + nS; e += G) F[e] = 0.0;
   group_sync<G>(bar);
 
-  // (1) extend-add: sources in fixed order, no atomics
+  // (1) extend-add through the scatter table: sources in fixed order, no atomics
+  const int* sc = L.maps + L.pat[(size_t)L.pattern_of[f] * TF_PAT_WIDTH + TF_PAT_SOFF];
   for (int c = 0; c < S.nsrc; c++) {
     const int len = c == 0 ? S.len0 : S.len1;
-    const int* cm = mp + (c == 0 ? 0 : S.len0);
     const int n = (int)tri32(len, 0);
-    int beg, end;
-    chunk_of(n, G, t, beg, end);
-    if (beg < end) {
-      int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
-      if (L.is_leaf) {
-        const double* E = src0;
+    const int* scc = sc + (c == 0 ? 0 : (int)tri32(S.len0, 0));
+    if (L.is_leaf) {  // dense len x len element matrix, lower part
+      int beg, end;
+      chunk_of(n, G, t, beg, end);
+      if (beg < end) {
+        int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
         for (int e = beg; e < end; e++) {
-          const int R = cm[a], C = cm[b];
-          F[R > C ? tri32(R, C) : tri32(C, R)] += E[a * L.elem_ld + b];
-          if (++b > a) { a++; b = 0; }
-        }
-      } else {
-        const double* src = c == 0 ? src0 : src1;
-        constexpr int U = 4;
-        int e = beg;
-        for (; e + U <= end; e += U) {
-          double v[U];
-#pragma unroll
-          for (int q = 0; q < U; q++) v[q] = src[e + q];
-#pragma unroll
-          for (int q = 0; q < U; q++) {
-            const int R = cm[a], C = cm[b];
-            F[R > C ? tri32(R, C) : tri32(C, R)] += v[q];
-            if (++b > a) { a++; b = 0; }
-          }
-        }
-        for (; e < end; e++) {
-          const int R = cm[a], C = cm[b];
-          F[R > C ? tri32(R, C) : tri32(C, R)] += src[e];
+          F[__ldg(scc + e)] += src0[a * L.elem_ld + b];
           if (++b > a) { a++; b = 0; }
         }
       }
+    } else {
+      const double* src = c == 0 ? src0 : src1;
+      for (int e = t; e < n; e += G) F[__ldg(scc + e)] += src[e];
     }
     group_sync<G>(bar);
   }
@@ -97,34 +92,35 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
   for (int c = 0; c < k; c++) {
     const double d = F[tri32(c, c)];
     if (t == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-    for (int r = c + 1 + t; r < m; r += G) lv[r] = F[tri32(r, c)] / d;
+    for (int r = c + 1 + t; r < m; r += G) lv[r] = F[rowp(r) + c] / d;
     group_sync<G>(bar);
     for (int r = c + 1 + t; r < m; r += G) {
-      double* row = F + tri32(r, 0);
+      double* row = F + rowp(r);
       const double frc = row[c];
       const int smax = min(r, k - 1);
-      for (int s = c + 1; s <= smax; s++) row[s] -= lv[s] * frc;
+      for (int q = c + 1; q <= smax; q++) row[q] -= lv[q] * frc;
       row[c] = lv[r];
     }
     group_sync<G>(bar);
   }
 
-  // (3) Schur block: F[k+i][k+j] -= sum_t l(k+i,t) d_t l(k+j,t), i >= j
+  // (3) Schur block: S[i][j] -= sum_q L21[i][q] d_q L21[j][q], i >= j
   if (k > 0 && u > 0) {
     for (int c = t; c < k; c += G) lv[c] = F[tri32(c, c)];  // pivots
     group_sync<G>(bar);
+    const double* P21 = F + tk;
     if constexpr (G >= 32) {
       const int warp = t >> 5, lane = t & 31, g8 = lane >> 2, tq = lane & 3;
       const int T = (u + 7) >> 3, ntile = T * (T + 1) / 2;
       for (int tile = warp; tile < ntile; tile += G / 32) {
         int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-        while (I * (I + 1) / 2 > tile) I--;
-        while ((I + 1) * (I + 2) / 2 <= tile) I++;
+        I -= (I * (I + 1) / 2 > tile);
+        I += ((I + 1) * (I + 2) / 2 <= tile);
         const int J = tile - I * (I + 1) / 2;
-        const int ra = k + 8 * I + g8, rb = k + 8 * J + g8;
-        const double* arow = F + tri32(min(ra, m - 1), 0);
-        const double* brow = F + tri32(min(rb, m - 1), 0);
-        const bool va = ra < m, vb = rb < m;
+        const int ia = 8 * I + g8, ib = 8 * J + g8;
+        const double* arow = P21 + min(ia, u - 1) * ks;
+        const double* brow = P21 + min(ib, u - 1) * ks;
+        const bool va = ia < u, vb = ib < u;
         double acc[2] = {0.0, 0.0};
         for (int kk = 0; kk < k; kk += 4) {
           const int q = kk + tq;
@@ -132,24 +128,23 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
           const double bv = (vb && q < k) ? brow[q] : 0.0;
           dmma884(acc, av, bv);
         }
-        const int R = k + 8 * I + g8;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          const int Cc = k + 8 * J + 2 * tq + h;
-          if (R < m && Cc <= R) F[tri32(R, Cc)] -= acc[h];
+          const int jc = 8 * J + 2 * tq + h;
+          if (ia < u && jc <= ia) Sb[tri32(ia, jc)] -= acc[h];
         }
       }
     } else {
       int beg, end;
-      chunk_of((int)tri32(u, 0), G, t, beg, end);
+      chunk_of(nS, G, t, beg, end);
       if (beg < end) {
         int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
         for (int e = beg; e < end; e++) {
-          const double* ra = F + tri32(k + a, 0);
-          const double* rb = F + tri32(k + b, 0);
+          const double* ra = P21 + a * ks;
+          const double* rb = P21 + b * ks;
           double acc = 0.0;
           for (int q = 0; q < k; q++) acc += ra[q] * lv[q] * rb[q];
-          F[tri32(k + a, k + b)] -= acc;
+          Sb[e] -= acc;
           if (++b > a) { a++; b = 0; }
         }
       }
@@ -157,31 +152,19 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
     group_sync<G>(bar);
   }
 
-  // (4) copy-out: factor slot (panel rows, lower part, + pivots) and Schur block
+  // (4) copy-out: factor slot (panel m x kp + pivots) and the packed Schur block
   if (k > 0) {
-    int beg, end;
-    chunk_of(m * k, G, t, beg, end);
-    if (beg < end) {
-      int r = beg / k, c = beg - r * k;
-      for (int e = beg; e < end; e++) {
-        if (c <= r) fac_out[(long long)r * kp + c] = F[tri32(r, c)];
-        if (++c == k) { c = 0; r++; }
-      }
+    for (int e = t; e < k * kp; e += G) {  // pivot block rows: packed -> dense
+      const int r = e / kp, c = e - r * kp;
+      fac_out[e] = c <= r ? F[tri32(r, c)] : 0.0;
     }
-    double* dv = fac_out + (long long)m * kp;
-    for (int c = t; c < kp; c += G) dv[c] = c < k ? F[tri32(c, c)] : 0.0;
-  }
-  if (u > 0) {
-    int beg, end;
-    chunk_of((int)tri32(u, 0), G, t, beg, end);
-    if (beg < end) {
-      int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
-      for (int e = beg; e < end; e++) {
-        upd_dst[e] = F[tri32(k + a, k + b)];
-        if (++b > a) { a++; b = 0; }
-      }
+    for (int e = t; e < u * kp; e += G) {  // L21 rows: stride ks -> kp
+      const int r = e / kp, c = e - r * kp;
+      fac_out[k * kp + e] = F[tk + r * ks + c];
     }
+    for (int c = t; c < kp; c += G) fac_out[m * kp + c] = c < k ? F[tri32(c, c)] : 0.0;
   }
+  for (int e = t; e < nS; e += G) upd_dst[e] = Sb[e];
 }
 
 template <int G, int GPC>
@@ -197,28 +180,20 @@ __global__ void __launch_bounds__(G* GPC)
   if (f >= L.n_fronts) return;  // whole group exits; syncs are group-local
   unsigned char* my = smem_raw + (size_t)gid * smem_per_group;
   double* F = reinterpret_cast<double*>(my);
-  double* lv = F + tri32(L.max_m, 0);
-  int* mp = reinterpret_cast<int*>(lv + L.max_m);
+  double* lv = F + small_front_doubles(L.max_m, L.max_k) - L.max_m;
   const Shape S = front_shape(L, f);
   const double* s0 = L.is_leaf ? elem + f * L.elem_stride
                                : child_upd + L.child_slot(f, 0) * L.child_upd_stride;
   const double* s1 = L.is_leaf ? nullptr : child_upd + L.child_slot(f, 1) * L.child_upd_stride;
-  factor_front<G>(L, f, S, s0, s1, F, lv, mp, factors + f * L.fac_stride,
+  factor_front<G>(L, f, S, s0, s1, F, lv, factors + f * L.fac_stride,
                   upd_out + f * L.upd_stride, threshold, err, t, 1 + gid);
-}
-
-int small_smem_per_group(int max_m) {
-  size_t bytes = sizeof(double) * ((size_t)max_m * (max_m + 1) / 2 + max_m) +
-                 sizeof(int) * 2 * (size_t)max_m;
-  bytes = (bytes + 15) & ~(size_t)15;
-  return (int)bytes;
 }
 
 template <int G, int GPC>
 static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, const double* elem,
                                   double* factors, double* upd_out, double thr,
                                   unsigned long long* err, cudaStream_t st) {
-  const int per = small_smem_per_group(L.max_m);
+  const int per = small_smem_per_group(L.max_m, L.max_k);
   const size_t smem = (size_t)per * GPC;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = factor_small_kernel<G, GPC>;
@@ -281,8 +256,7 @@ __global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
   for (int L = 0; L < A.nlev; L++) {
     const LevelArgs& lv = A.lv[L];
     double* F = reinterpret_cast<double*>(ws);
-    double* lvec = F + tri32(lv.max_m, 0);
-    int* mp = reinterpret_cast<int*>(lvec + lv.max_m);
+    double* lvec = F + small_front_doubles(lv.max_m, lv.max_k) - lv.max_m;
     double* prev = arena[(L + 1) & 1];
     double* cur = arena[L & 1];
     const int cst = L > 0 ? (int)tri32(A.lv[L - 1].max_upd, 0) : 0;
@@ -295,7 +269,7 @@ __global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
       const double* s0 = lv.is_leaf ? elem + f * lv.elem_stride : prev + (2 * i) * cst;
       const double* s1 = lv.is_leaf ? nullptr : prev + (2 * i + 1) * cst;
       double* dst = L == top ? upd_out + f * lv.upd_stride : cur + i * ost;
-      factor_front<kSubG>(lv, f, S, s0, s1, F, lvec, mp, A.fac[L] + f * lv.fac_stride, dst,
+      factor_front<kSubG>(lv, f, S, s0, s1, F, lvec, A.fac[L] + f * lv.fac_stride, dst,
                           threshold, err, t, 0);
       group_sync<kSubG>(0);
     }
@@ -304,10 +278,10 @@ __global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
 
 // Shared-memory plan of one subtree group; 0 when the levels cannot be fused.
 static size_t subtree_group_bytes(const LevelArgs* lv, int nlev, int arena[2], int* ws) {
-  int mm = 1;
+  int ws_max = 16;
   arena[0] = arena[1] = 0;
   for (int L = 0; L < nlev; L++) {
-    mm = std::max(mm, lv[L].max_m);
+    ws_max = std::max(ws_max, small_smem_per_group(lv[L].max_m, lv[L].max_k));
     if (L < nlev - 1) {
       const int nf = 1 << (nlev - 1 - L);
       arena[L & 1] = std::max(arena[L & 1], nf * (int)tri32(lv[L].max_upd, 0));
@@ -315,7 +289,7 @@ static size_t subtree_group_bytes(const LevelArgs* lv, int nlev, int arena[2], i
   }
   arena[0] = (arena[0] + 1) & ~1;
   arena[1] = (arena[1] + 1) & ~1;
-  *ws = small_smem_per_group(mm);
+  *ws = ws_max;
   return sizeof(double) * (arena[0] + arena[1]) + *ws;
 }
 

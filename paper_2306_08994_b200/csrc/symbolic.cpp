@@ -29,6 +29,8 @@ namespace {
 
 inline int bitlen64(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
 
+constexpr int32_t kScatterMaxM = 232;  // = kSmallMaxM of the shared-memory kernels
+
 struct Level {
   int32_t n_fronts = 0, n_patterns = 0, max_m = 0, max_k = 0, max_upd = 0;
   int64_t node_base = 0, piv_base = 0, n_pivots = 0;
@@ -341,8 +343,28 @@ extern "C" int tf_plan_create(int64_t n_dof, int64_t n_elem, const int64_t* elem
           for (int32_t a = 0; a < len; a++) lv.maps[ioff + (size_t)c * fm[i] + fwd[a]] = a;
         }
         const int32_t kp = (fk[i] + 3) & ~3;
+        // scatter table for the shared-memory front kernels (small fronts)
+        int32_t soff = -1;
+        if (fm[i] <= kScatterMaxM) {
+          soff = (int32_t)lv.maps.size();
+          const int64_t m = fm[i], k = fk[i], u = m - k, tk = k * (k + 1) / 2, ks = kp + 1;
+          auto pos = [&](int64_t R, int64_t C) -> int32_t {  // C <= R
+            if (R < k) return (int32_t)(R * (R + 1) / 2 + C);
+            if (C < k) return (int32_t)(tk + (R - k) * ks + C);
+            return (int32_t)(tk + u * ks + (R - k) * (R - k + 1) / 2 + (C - k));
+          };
+          for (int c = 0; c < nsrc; c++) {
+            const int32_t* fwd = fmap.data() + mptr[i] + (c == 0 ? 0 : len0);
+            const int32_t len = c == 0 ? len0 : len1;
+            for (int32_t a = 0; a < len; a++)
+              for (int32_t b = 0; b <= a; b++) {
+                const int64_t R = std::max(fwd[a], fwd[b]), C = std::min(fwd[a], fwd[b]);
+                lv.maps.push_back(pos(R, C));
+              }
+          }
+        }
         int32_t row[TF_PAT_WIDTH] = {fm[i], fk[i], nsrc, len0, len1, off0, off0 + len0,
-                                     L == 0 ? 1 : 0, ioff, kp, fm[i] * kp + kp, 0};
+                                     L == 0 ? 1 : 0, ioff, kp, fm[i] * kp + kp, soff};
         lv.pat.insert(lv.pat.end(), row, row + TF_PAT_WIDTH);
         bucket.push_back(found);
         lv.max_m = std::max(lv.max_m, fm[i]);
