@@ -47,7 +47,7 @@ __device__ __forceinline__ double child_entry(const double* __restrict__ src, in
 }
 __global__ void __launch_bounds__(32 * kAsmWarps)
     large_assemble_kernel(LevelArgs L, const double* __restrict__ child_upd,
-                          double* __restrict__ factors, double* __restrict__ upd) {
+                          double* __restrict__ factors, double* __restrict__ upd, int with_s) {
   const long long f = blockIdx.x;  // fronts on x (no 65535 limit), row groups on y
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(32 * kAsmWarps)
       }
       prow[c] = v;
     }
-    if (r >= k) {
+    if (with_s && r >= k) {  // else the Schur kernel assembles S in its epilogue
       const int a = r - k;
       double* srow = Sf + tri32(a, 0);
       for (int c = lane; c <= a; c += 32) {
@@ -538,7 +538,9 @@ struct GemmCfg {
 template <int MODE, class G>
 __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double* factors,
                                                             double* upd, int row0, int col0,
-                                                            int col1, int t0, int t1) {
+                                                            int col1, int t0, int t1,
+                                                            const double* __restrict__ child_upd,
+                                                            int asm_s) {
   constexpr int BM = G::BM, BN = G::BN, BK = G::BK, ST = G::ST, LD = G::LD;
   constexpr int MI = G::MI, NJ = G::NJ;
   extern __shared__ __align__(16) double gsm[];
@@ -591,7 +593,10 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
     bK0 = 0;
     kLen = kb;
   }
-  if (kLen <= 0) return;
+  if (kLen <= 0) {
+    if (!(MODE == 1 && asm_s)) return;
+    kLen = 0;  // no pivots in this front: S is its assembled block
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wy = warp / G::WC, wx = warp % G::WC;  // WR x WC warps
   const int nk = (kLen + BK - 1) / BK;
@@ -678,6 +683,42 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
   cp_async_wait<0>();
   if (MODE == 2) __syncthreads();  // every A tile row is read before it is overwritten
   double* out = MODE == 1 ? upd + f * L.upd_stride : Pf;
+  if (MODE == 1 && asm_s) {
+    // S = (children's contributions, gathered through the inverse extend-add
+    // maps: the assembly of S fused here) - L21 D L21^T; one write per entry
+    const int* inv0 = L.maps + s.ioff;
+    const int* inv1 = inv0 + m;
+    const bool two = s.nsrc == 2;
+    const double* src0 = child_upd + L.child_slot(f, 0) * L.child_upd_stride;
+    const double* src1 = child_upd + L.child_slot(f, 1) * L.child_upd_stride;
+#pragma unroll
+    for (int i = 0; i < MI; i++) {
+      const int rl = wy * G::WM + i * 8 + (lane >> 2);
+      if (rl >= nA) continue;
+      const int R = (int)tile_r0 + rl;
+      const int a0 = inv0[k + R], ta0 = a0 >= 0 ? tri32(a0, 0) : 0;
+      const int a1 = two ? inv1[k + R] : -1, ta1 = a1 >= 0 ? tri32(a1, 0) : 0;
+      double* orow = out + tri32(R, 0);
+#pragma unroll
+      for (int j = 0; j < NJ; j++) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cl = wx * G::WN + j * 8 + 2 * (lane & 3) + h;
+          const int C = (int)tile_c0 + cl;
+          if (cl >= nB || C > R) continue;
+          double v = 0.0;
+          const int b0 = inv0[k + C];
+          if (a0 >= 0 && b0 >= 0) v = src0[a0 >= b0 ? ta0 + b0 : tri32(b0, a0)];
+          if (two) {
+            const int b1 = inv1[k + C];
+            if (a1 >= 0 && b1 >= 0) v += src1[a1 >= b1 ? ta1 + b1 : tri32(b1, a1)];
+          }
+          orow[C] = v - acc[i][j][h];
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < MI; i++) {
     const int rl = wy * G::WM + i * 8 + (lane >> 2);
@@ -707,10 +748,6 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
 using GTrsm = GemmCfg<64, 64, 16, 2>;   // N = 64 = one diagonal block
 using GPanel = GemmCfg<64, 64, 16, 2>;
 using GSchurA = GemmCfg<64, 64, 16, 2>;        // 8 warps of 16x32
-using GSchurB = GemmCfg<64, 64, 8, 4>;
-using GSchurC = GemmCfg<64, 64, 16, 3, 2, 2>;  // 4 warps of 32x32
-using GSchurD = GemmCfg<64, 32, 16, 3, 4, 1>;  // 4 warps of 16x32
-using GSchurE = GemmCfg<128, 64, 16, 3>;
 
 template <int MODE, class G>
 static void gemm_attr() {
@@ -724,11 +761,13 @@ static void gemm_attr() {
 
 template <class G>
 static void launch_schur(const LevelArgs& L, double* factors, double* upd_out, cudaStream_t st,
-                         int t0 = 0, int t1 = 0) {
+                         int t0 = 0, int t1 = 0, const double* child_upd = nullptr) {
+  // child_upd != nullptr: S is assembled in the epilogue (not by the assembly kernel)
   gemm_attr<1, G>();
   dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + G::BN - 1) / G::BN),
          (unsigned)((L.max_upd + G::BM - 1) / G::BM));
-  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, t0, t1);
+  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, t0, t1,
+                                                         child_upd, child_upd ? 1 : 0);
 }
 
 // P[r][c] -= sum_{t in [t0, t1)} l_rt d_t l_ct for c in [c0, c1), r >= c.
@@ -739,18 +778,10 @@ static void launch_panel_update(const LevelArgs& L, double* factors, int c0, int
   gemm_attr<0, GPanel>();
   timer_begin(K_PANEL, st);
   large_update_kernel<0, GPanel><<<g, GPanel::NT, GPanel::smem, st>>>(L, factors, nullptr, c0, c0,
-                                                                      c1, t0, t1);
+                                                                      c1, t0, t1, nullptr, 0);
   timer_end(st);
 }
 
-static int gemm_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TFB_SCHUR_CFG");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
 
 static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
                                 unsigned long long* err, int a, int b, cudaStream_t st) {
@@ -774,7 +805,7 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
       gemm_attr<2, GTrsm>();
       timer_begin(K_TRSM, st);
       large_update_kernel<2, GTrsm><<<g, GTrsm::NT, GTrsm::smem, st>>>(L, factors, nullptr, 0, 0, 0,
-                                                                   a, 0);
+                                                                   a, 0, nullptr, 0);
       timer_end(st);
     }
     return cudaGetLastError();
@@ -878,6 +909,10 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                          (int)kDiagSmem);
     attr = true;
   }
+  const bool lookahead = L.max_k > kLookaheadCols && L.level_fronts <= kLookaheadMaxFronts;
+  // S is assembled by the Schur kernel's epilogue unless the level has no
+  // pivots or updates S in several chunks (lookahead)
+  const bool fused_s = L.max_k > 0 && L.max_upd > 0 && !lookahead;
   {
     // ~kAsmRowsPerWarp rows per warp, but at least ~8 CTAs per SM on levels
     // with few (large) fronts, down to one row per warp
@@ -886,27 +921,20 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
     const long long cap = (L.max_m + kAsmWarps - 1) / kAsmWarps;
     const unsigned gy = (unsigned)std::max(1LL, std::min(std::max(by_rows, by_sms), cap));
     timer_begin(K_ASSEMBLE, st);
-    large_assemble_kernel<<<dim3(L.n_fronts, gy), 32 * kAsmWarps, 0, st>>>(L, child_upd, factors,
-                                                                           upd_out);
+    large_assemble_kernel<<<dim3(L.n_fronts, gy), 32 * kAsmWarps, 0, st>>>(
+        L, child_upd, factors, upd_out, fused_s ? 0 : 1);
     timer_end(st);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (L.max_k > kLookaheadCols && L.level_fronts <= kLookaheadMaxFronts)
-    return factor_lookahead(L, factors, upd_out, thr, err, st);
+  if (lookahead) return factor_lookahead(L, factors, upd_out, thr, err, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);
     if (e != cudaSuccess) return e;
   }
-  if (L.max_upd > 0 && L.max_k > 0) {
+  if (fused_s) {
     timer_begin(K_SCHUR, st);
-    switch (gemm_variant()) {
-      case 1: launch_schur<GSchurB>(L, factors, upd_out, st); break;
-      case 2: launch_schur<GSchurC>(L, factors, upd_out, st); break;
-      case 3: launch_schur<GSchurD>(L, factors, upd_out, st); break;
-      case 4: launch_schur<GSchurE>(L, factors, upd_out, st); break;
-      default: launch_schur<GSchurA>(L, factors, upd_out, st); break;
-    }
+    launch_schur<GSchurA>(L, factors, upd_out, st, 0, 0, child_upd);
     timer_end(st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
