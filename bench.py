@@ -46,6 +46,16 @@ FP64_PEAK_TFLOPS = 35.47  # measured cuBLAS DGEMM on this pool: profiles/r01_dge
 CPU_SAMPLE = dict(shape=(128, 128), degree=1)
 
 
+def measured_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (tools/ncu_traffic.py -> profiles/traffic_<config>.json), else None."""
+    try:
+        d = json.loads((ROOT / "profiles" / f"traffic_{config}.json").read_text())
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -288,7 +298,9 @@ def run_ours(args, cfg):
             sf = float(((m_ - k_) * (m_ - k_ + 1) * k_).sum())
             schur_flops += sf
             panel_flops += st["ldl_flops"] - sf
-            asm_bytes += st["bytes"] - 8.0 * st["upd_entries"] + 8.0 * st["upd_entries"]
+            # the Schur epilogue writes S (fused assembly): the assembly kernel
+            # reads the children and writes the panel
+            asm_bytes += st["bytes"] - 8.0 * st["upd_entries"]
         else:
             small_bytes += st["bytes"]
     work = {  # algorithmic work per step of each kernel class
@@ -311,7 +323,7 @@ def run_ours(args, cfg):
         roof = {"bound": "tensor", "achieved": per_launch / t_launch / 1e12,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = measured_traffic(args.config, name)
     roof["kernel"] = name
     roof["launches_per_step"] = k_n / args.steps
     roof["share_of_kernel_time"] = k_ms / max(tot_ms, 1e-9)

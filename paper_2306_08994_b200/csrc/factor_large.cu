@@ -547,7 +547,18 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
   double* As = gsm;                       // [ST][BM][LD]
   double* Bs = As + ST * BM * LD;         // [ST][BN][LD]
   double* Ds = Bs + ST * BN * LD;         // [ST][BK]
-  const long long f = blockIdx.x;
+  // MODE 1: 1-D grid over (front, lower-triangular tile (I, J)) in row-major
+  // tile order, so co-resident CTAs share L21 row tiles in L2 (col0 = tiles
+  // per dimension); other modes: fronts on x
+  long long f = blockIdx.x;
+  int tI = 0, tJ = 0;
+  if (MODE == 1) {
+    const long long ntf = (long long)col0 * (col0 + 1) / 2;
+    f = (long long)blockIdx.x / ntf;
+    const int t = (int)((long long)blockIdx.x - f * ntf);
+    tI = tri_row32(t);
+    tJ = t - (int)tri32(tI, 0);
+  }
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   double* Pf = factors + f * L.fac_stride;
@@ -568,9 +579,9 @@ __global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double
     kLen = min(t1, k) - t0;
   } else if (MODE == 1) {
     const int u = m - k;
-    tile_r0 = (long long)blockIdx.z * BM;
-    tile_c0 = (long long)blockIdx.y * BN;
-    if (tile_r0 >= u || tile_c0 >= u || tile_r0 + BM <= tile_c0) return;
+    tile_r0 = (long long)tI * BM;
+    tile_c0 = (long long)tJ * BN;
+    if (tile_r0 >= u) return;
     aRow0 = k + (int)tile_r0;
     bRow0 = k + (int)tile_c0;
     nA = min(BM, u - (int)tile_r0);
@@ -763,11 +774,12 @@ template <class G>
 static void launch_schur(const LevelArgs& L, double* factors, double* upd_out, cudaStream_t st,
                          int t0 = 0, int t1 = 0, const double* child_upd = nullptr) {
   // child_upd != nullptr: S is assembled in the epilogue (not by the assembly kernel)
+  static_assert(G::BM == G::BN, "square Schur tiles");
   gemm_attr<1, G>();
-  dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_upd + G::BN - 1) / G::BN),
-         (unsigned)((L.max_upd + G::BM - 1) / G::BM));
-  large_update_kernel<1, G><<<g, G::NT, G::smem, st>>>(L, factors, upd_out, 0, 0, 0, t0, t1,
-                                                         child_upd, child_upd ? 1 : 0);
+  const int T = (L.max_upd + G::BM - 1) / G::BM;
+  const long long grid = (long long)L.n_fronts * T * (T + 1) / 2;
+  large_update_kernel<1, G><<<(unsigned)grid, G::NT, G::smem, st>>>(
+      L, factors, upd_out, 0, T, 0, t0, t1, child_upd, child_upd ? 1 : 0);
 }
 
 // P[r][c] -= sum_{t in [t0, t1)} l_rt d_t l_ct for c in [c0, c1), r >= c.
