@@ -87,19 +87,29 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
     group_sync<G>(bar);
   }
 
-  // (2) panel: right-looking over the k pivot columns, updates confined to them
+  // (2) panel: right-looking over the k pivot columns, updates confined to
+  // them, columns kept unscaled during the sweep (a(r,q) -= a(r,c) a(q,c) / d_c
+  // reads only finished column-c entries: one barrier per pivot), then scaled.
   const long long piv0 = L.piv_off[f];
   for (int c = 0; c < k; c++) {
     const double d = F[tri32(c, c)];
     if (t == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
-    for (int r = c + 1 + t; r < m; r += G) lv[r] = F[rowp(r) + c] / d;
-    group_sync<G>(bar);
+    const double dinv = 1.0 / d;
     for (int r = c + 1 + t; r < m; r += G) {
       double* row = F + rowp(r);
-      const double frc = row[c];
+      const double lrc = row[c] * dinv;
       const int smax = min(r, k - 1);
-      for (int q = c + 1; q <= smax; q++) row[q] -= lv[q] * frc;
-      row[c] = lv[r];
+      for (int q = c + 1; q <= smax; q++) row[q] -= lrc * F[tri32(q, c)];
+    }
+    group_sync<G>(bar);
+  }
+  if (k > 0) {
+    for (int c = t; c < k; c += G) lv[c] = 1.0 / F[tri32(c, c)];
+    group_sync<G>(bar);
+    for (int r = 1 + t; r < m; r += G) {  // l(r, c) = a(r, c) / d_c
+      double* row = F + rowp(r);
+      const int cm = min(r, k);
+      for (int c = 0; c < cm; c++) row[c] *= lv[c];
     }
     group_sync<G>(bar);
   }
