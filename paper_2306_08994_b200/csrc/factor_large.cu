@@ -841,8 +841,16 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
 //   schur  (low priority) : S -= L21_j D_j L21_j^T
 // Every entry is updated by the super-blocks in increasing order, as in the
 // sequential path, so results are identical run to run.
-constexpr int kLookaheadCols = 256;
-constexpr int kLookaheadMaxFronts = 128;
+static int lookahead_cols() {  // super-block width (TFB_LOOKAHEAD_COLS for tuning sweeps)
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TFB_LOOKAHEAD_COLS");
+    v = e ? std::max(64, atoi(e) / 64 * 64) : 256;
+  }
+  return v;
+}
+#define kLookaheadCols lookahead_cols()
+constexpr int kLookaheadMaxFronts = 16;  // measured: L18-L19 (32-64 fronts) faster without
 
 struct LookaheadStreams {
   cudaStream_t chain = nullptr, panel = nullptr, schur = nullptr;
