@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libtfb200.so"
+LIB_PATH = Path(os.environ.get("TFB_LIB", Path(__file__).resolve().parent / "libtfb200.so"))
 
 TF_OK = 0
 TF_ZERO_PIVOT = 2
