@@ -850,6 +850,17 @@ static int lookahead_cols() {  // super-block width (TFB_LOOKAHEAD_COLS for tuni
   return v;
 }
 #define kLookaheadCols lookahead_cols()
+// Levels without a Schur block (the root) have only the chain and the panel
+// updates: narrower super-blocks shorten the chain (TFB_LOOKAHEAD_ROOT_COLS).
+static int lookahead_root_cols() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TFB_LOOKAHEAD_ROOT_COLS");
+    v = e ? std::max(64, atoi(e) / 64 * 64) : 128;  // measured best on the cfg5 root
+  }
+  return v;
+}
+static int lookahead_width(int max_upd) { return max_upd > 0 ? lookahead_cols() : lookahead_root_cols(); }
 constexpr int kLookaheadMaxFronts = 16;  // measured: L18-L19 (32-64 fronts) faster without
 
 struct LookaheadStreams {
@@ -877,11 +888,12 @@ static cudaError_t factor_lookahead(const LevelArgs& L, double* factors, double*
   cudaStreamWaitEvent(S.chain, S.start, 0);
   cudaStreamWaitEvent(S.panel, S.start, 0);
   cudaStreamWaitEvent(S.schur, S.start, 0);
-  const int nsb = (L.max_k + kLookaheadCols - 1) / kLookaheadCols;
+  const int W = lookahead_width(L.max_upd);
+  const int nsb = (L.max_k + W - 1) / W;
   const bool schur = L.max_upd > 0;
   for (int j = 0; j < nsb; j++) {
-    const int c0 = j * kLookaheadCols, c1 = std::min(c0 + kLookaheadCols, L.max_k);
-    const int c2 = std::min(c1 + kLookaheadCols, L.max_k);
+    const int c0 = j * W, c1 = std::min(c0 + W, L.max_k);
+    const int c2 = std::min(c1 + W, L.max_k);
     cudaError_t e = panel_factor(L, factors, thr, err, c0, c1, S.chain);
     if (e != cudaSuccess) return e;
     if (j + 1 < nsb) {
@@ -929,7 +941,8 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                          (int)kDiagSmem);
     attr = true;
   }
-  const bool lookahead = L.max_k > kLookaheadCols && L.level_fronts <= kLookaheadMaxFronts;
+  const bool lookahead =
+      L.max_k > lookahead_width(L.max_upd) && L.level_fronts <= kLookaheadMaxFronts;
   // S is assembled by the Schur kernel's epilogue unless the level has no
   // pivots or updates S in several chunks (lookahead)
   const bool fused_s = L.max_k > 0 && L.max_upd > 0 && !lookahead;
@@ -984,11 +997,12 @@ int large_panel_launches(int max_k, int n_fronts) {
 // Kernel launches of one launch_factor_large call (tf_level_launch_count).
 int large_level_launches(int max_k, int max_upd, long long level_fronts) {
   const int fronts = (int)std::min<long long>(level_fronts, 1 << 30);
-  if (max_k > kLookaheadCols && level_fronts <= kLookaheadMaxFronts) {
-    const int nsb = (max_k + kLookaheadCols - 1) / kLookaheadCols;
+  const int W = lookahead_width(max_upd);
+  if (max_k > W && level_fronts <= kLookaheadMaxFronts) {
+    const int nsb = (max_k + W - 1) / W;
     int n = 2;  // assembly, finalize
     for (int j = 0; j < nsb; j++) {
-      const int c0 = j * kLookaheadCols, c1 = std::min(c0 + kLookaheadCols, max_k);
+      const int c0 = j * W, c1 = std::min(c0 + W, max_k);
       n += large_panel_launches(c1 - c0, fronts) + (j + 1 < nsb) + (j + 2 < nsb) + (max_upd > 0);
     }
     return n;
