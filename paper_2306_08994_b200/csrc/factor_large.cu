@@ -536,7 +536,7 @@ struct GemmCfg {
 };
 
 template <int MODE, class G>
-__global__ void __launch_bounds__(G::NT) large_update_kernel(LevelArgs L, double* factors,
+__global__ void __launch_bounds__(G::NT, 4) large_update_kernel(LevelArgs L, double* factors,
                                                             double* upd, int row0, int col0,
                                                             int col1, int t0, int t1,
                                                             const double* __restrict__ child_upd,

@@ -11,7 +11,11 @@ ap.add_argument("--shape", default="1024,1024")
 ap.add_argument("--degree", type=int, default=1)
 ap.add_argument("--nrhs", type=int, default=1)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--small-max-m", type=int, default=None)
 a = ap.parse_args()
+if a.small_max_m is not None:
+    from paper_2306_08994_b200.device import set_small_front_limit
+    set_small_front_limit(a.small_max_m)
 shape = tuple(int(x) for x in a.shape.split(","))
 t0 = time.time()
 mesh = tf.TensorMesh(shape, a.degree)
