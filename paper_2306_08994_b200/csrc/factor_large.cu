@@ -881,7 +881,8 @@ static LookaheadStreams& lookahead_streams() {
   return ls;
 }
 
-static cudaError_t factor_lookahead(const LevelArgs& L, double* factors, double* upd_out,
+static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd, double* factors,
+                                    double* upd_out,
                                     double thr, unsigned long long* err, cudaStream_t st) {
   LookaheadStreams& S = lookahead_streams();
   cudaEventRecord(S.start, st);  // after the assembly
@@ -910,7 +911,8 @@ static cudaError_t factor_lookahead(const LevelArgs& L, double* factors, double*
     if (schur) {
       cudaStreamWaitEvent(S.schur, S.chain_done, 0);
       timer_begin(K_SCHUR, S.schur);
-      launch_schur<GSchurA>(L, factors, upd_out, S.schur, c0, c1);
+      // the first chunk also assembles S (children gathered in its epilogue)
+      launch_schur<GSchurA>(L, factors, upd_out, S.schur, c0, c1, j == 0 ? child_upd : nullptr);
       timer_end(S.schur);
     }
   }
@@ -943,9 +945,9 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   }
   const bool lookahead =
       L.max_k > lookahead_width(L.max_upd) && L.level_fronts <= kLookaheadMaxFronts;
-  // S is assembled by the Schur kernel's epilogue unless the level has no
-  // pivots or updates S in several chunks (lookahead)
-  const bool fused_s = L.max_k > 0 && L.max_upd > 0 && !lookahead;
+  // S is assembled by the (first) Schur kernel's epilogue unless the level
+  // has no pivots
+  const bool fused_s = L.max_k > 0 && L.max_upd > 0;
   {
     // ~kAsmRowsPerWarp rows per warp, but at least ~8 CTAs per SM on levels
     // with few (large) fronts, down to one row per warp
@@ -960,7 +962,7 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (lookahead) return factor_lookahead(L, factors, upd_out, thr, err, st);
+  if (lookahead) return factor_lookahead(L, child_upd, factors, upd_out, thr, err, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);
     if (e != cudaSuccess) return e;
