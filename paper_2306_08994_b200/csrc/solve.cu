@@ -688,8 +688,8 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
       if (work <= 24 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(2, 64);
       else if (work <= 48 && bytes * 64 <= (long long)kSmallSolveSmem) e = TFB_SMALL(4, 64);
       else if (work <= 96 && bytes * 32 <= (long long)kSmallSolveSmem) e = TFB_SMALL(8, 32);
-      else if (work <= 256 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
-      else if (work <= 2048 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
+      else if (work <= 1024 && bytes * 8 <= (long long)kSmallSolveSmem) e = TFB_SMALL(32, 8);
+      else if (work <= 4096 && bytes * 2 <= (long long)kSmallSolveSmem) e = TFB_SMALL(128, 2);
       else e = TFB_SMALL(256, 1);
 #undef TFB_SMALL
     }
