@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(256)
   double* Mt = T + (nbuf - 1) * TB * TLD;      // M tile (aliases T when nbuf == 1)
   double* Xs = T + nbuf * TB * TLD;            // [TB][nr]
   double* Z = Xs + TB * nr;        // [TB][nr]
+  double* red = Z + TB * nr;       // [4][TB] (one column)
   const int tid = threadIdx.x;
   const long long nf = L.n_fronts;
   int* flx = flags;                                  // [nf][nb_max]: X_b final
@@ -551,11 +552,22 @@ __global__ void __launch_bounds__(256)
       for (int Rq = b + 2 + tid; Rq < rt; Rq += 256)
         while (ld_acquire(flp + (f * rt_max + Rq) * (long long)nb_max + b) == 0) __nanosleep(20);
       __syncthreads();
-      for (int e = tid; e < kb * nr; e += 256) {
-        double acc = Z[e];
-        for (int Rq = b + 2; Rq < rt; Rq++)
-          acc += __ldcg(part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB * nr + e);
-        Z[e] = acc;
+      if (ONE) {  // four interleaved partial sums per column, combined in fixed order
+        const int c = tid & (TB - 1), g = tid >> 6;
+        double acc = 0.0;
+        if (c < kb)
+          for (int Rq = b + 2 + g; Rq < rt; Rq += 4)
+            acc += __ldcg(part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB + c);
+        red[g * TB + c] = acc;
+        __syncthreads();
+        if (tid < kb) Z[tid] += ((red[tid] + red[TB + tid]) + red[2 * TB + tid]) + red[3 * TB + tid];
+      } else {
+        for (int e = tid; e < kb * nr; e += 256) {
+          double acc = Z[e];
+          for (int Rq = b + 2; Rq < rt; Rq++)
+            acc += __ldcg(part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB * nr + e);
+          Z[e] = acc;
+        }
       }
       // (c)
       if (rows1 > 0 && R1 < nb) wave_wait(flx + f * nb_max + R1);
@@ -789,7 +801,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
     const int nbuf = L.n_fronts <= kWaveFewFronts ? 2 : 1;
-    const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
+    const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr + 4 * TB);
     cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb * (1 + rt), st);
     timer_begin(K_SOLVE_BWD_BLOCK, st);
     if (nr == 1) {
