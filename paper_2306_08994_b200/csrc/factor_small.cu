@@ -20,6 +20,9 @@
 // Output per front: factor slot = panel P (m x kp row-major; P[r][c] = l(r,c)
 // for r > c, P[c][c] = d_c) followed by d (kp doubles); update slot = packed
 // lower (m-k)^2 Schur complement.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace tfb {
@@ -225,13 +228,33 @@ cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, con
                                 unsigned long long* err, cudaStream_t st) {
   // groups sized so that a CTA's shared memory stays small enough for several
   // CTAs per SM (occupancy hides the shared-memory latency of the pivot loop)
+  // (G, GPC) per front-order class m <= 4, 8, 16, 24, 48, 80, 232 (measured
+  // on B200, tools/small_sweep.sh); TFB_SMALL_CFG="G:GPC,..." overrides
+  static int cfg[7][2] = {{2, 128}, {4, 64}, {8, 32}, {16, 16}, {32, 4}, {128, 1}, {256, 1}};
+  static bool parsed = false;
+  if (!parsed) {
+    parsed = true;
+    if (const char* e = getenv("TFB_SMALL_CFG")) {
+      for (int i = 0; i < 7 && *e; i++) {
+        int g = 0, n = 0;
+        if (sscanf(e, "%d:%d", &g, &n) == 2) { cfg[i][0] = g; cfg[i][1] = n; }
+        while (*e && *e != ',') e++;
+        if (*e == ',') e++;
+      }
+    }
+  }
   const int mm = L.max_m;
-  if (mm <= 8) return launch_small_t<4, 64>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 16) return launch_small_t<8, 32>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 24) return launch_small_t<16, 16>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 48) return launch_small_t<32, 4>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  if (mm <= 80) return launch_small_t<128, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
-  return launch_small_t<256, 1>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  const int cls =
+      mm <= 4 ? 0 : mm <= 8 ? 1 : mm <= 16 ? 2 : mm <= 24 ? 3 : mm <= 48 ? 4 : mm <= 80 ? 5 : 6;
+  const int G = cfg[cls][0], GPC = cfg[cls][1];
+#define TFB_CASE(g, n) \
+  if (G == g && GPC == n) return launch_small_t<g, n>(L, child_upd, elem, factors, upd_out, thr, err, st);
+  TFB_CASE(2, 128) TFB_CASE(4, 64) TFB_CASE(4, 32) TFB_CASE(8, 32) TFB_CASE(8, 16)
+  TFB_CASE(16, 16) TFB_CASE(16, 8) TFB_CASE(32, 8) TFB_CASE(32, 4) TFB_CASE(32, 2)
+  TFB_CASE(64, 4) TFB_CASE(64, 2) TFB_CASE(64, 1) TFB_CASE(128, 2) TFB_CASE(128, 1)
+  TFB_CASE(256, 1)
+#undef TFB_CASE
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------- subtrees
