@@ -91,3 +91,46 @@ def test_large_tensor_plan_shapes():
     assert ms[:6] == [4, 6, 9, 13, 19, 27] and ks[-1] == ms[-1] == 257
     for lt in plan.native.levels:
         assert lt.n_patterns <= 40  # structured mesh: a handful of shape classes per level
+
+
+def test_scatter_tables_match_maps():
+    """TF_PAT_SOFF tables (shared-memory extend-add targets) agree with the
+    forward maps: entry (a, b) of source c lands at the layout position of
+    front cell (max(map[a], map[b]), min(...)) in [pivot rows packed | L21
+    rows of stride kp+1 | Schur block packed]; the Schur part is the update
+    slot's packed order; fronts above order 232 carry no table."""
+    from paper_2306_08994_b200 import _lib
+    mesh = tf.TensorMesh((24, 20), 2)
+    fronts = tf.generate_fronts(mesh)
+    tree = tf.build_elimination_tree(tf.sort_fronts(fronts), n_dof=mesh.n_dof)
+    plan = tf.symbolic_eliminate(tree, tf.assemble_system(mesh, "one"))
+    checked = 0
+    for lt in plan.native.levels:
+        for row in lt.pat:
+            m, k, kp = int(row[_lib.PAT_M]), int(row[_lib.PAT_K]), int(row[_lib.PAT_KP])
+            soff = int(row[_lib.PAT_SOFF])
+            if m > 232:
+                assert soff == -1
+                continue
+            ks, u, tk = kp + 1, m - k, k * (k + 1) // 2
+            seen = set()
+            pos = soff
+            for c in range(int(row[_lib.PAT_NSRC])):
+                ln = int(row[_lib.PAT_LEN0 + c])
+                fwd = lt.maps[int(row[_lib.PAT_OFF0 + c]):][:ln]
+                for a in range(ln):
+                    for b in range(a + 1):
+                        R, C = max(fwd[a], fwd[b]), min(fwd[a], fwd[b])
+                        if R < k:
+                            want = R * (R + 1) // 2 + C
+                        elif C < k:
+                            want = tk + (R - k) * ks + C
+                        else:
+                            want = tk + u * ks + (R - k) * (R - k + 1) // 2 + (C - k)
+                        assert lt.maps[pos] == want
+                        if c == 0:
+                            assert want not in seen  # one source never hits a cell twice
+                            seen.add(want)
+                        pos += 1
+                        checked += 1
+    assert checked > 1000
