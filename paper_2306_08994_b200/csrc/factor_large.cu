@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(G::NT, 4) large_update_kernel(LevelArgs L, dou
 // Tile shapes measured on B200 (tools/schur_sweep.sh): 64x64 tiles of 8 warps
 // with a 2-stage pipeline keep the most warps resident and win on every level.
 using GTrsm = GemmCfg<64, 64, 16, 2>;   // N = 64 = one diagonal block
+using GTrsm32 = GemmCfg<64, 32, 16, 2, 4, 1>;  // blocks of <= 32 columns: 4 warps of 16x32
 using GPanel = GemmCfg<64, 64, 16, 2>;
 using GSchurA = GemmCfg<64, 64, 16, 2>;        // 8 warps of 16x32
 
@@ -814,10 +815,16 @@ static cudaError_t panel_factor(const LevelArgs& L, double* factors, double thr,
         large_diag64_kernel<<<L.n_fronts, 256, kDiagSmem, st>>>(L, factors, a, thr, err);
       timer_end(st);
       dim3 g((unsigned)L.n_fronts, 1, (unsigned)((rows + GTrsm::BM - 1) / GTrsm::BM));
-      gemm_attr<2, GTrsm>();
       timer_begin(K_TRSM, st);
-      large_update_kernel<2, GTrsm><<<g, GTrsm::NT, GTrsm::smem, st>>>(L, factors, nullptr, 0, 0, 0,
-                                                                   a, 0, nullptr, 0);
+      if (b - a <= 32) {
+        gemm_attr<2, GTrsm32>();
+        large_update_kernel<2, GTrsm32><<<g, GTrsm32::NT, GTrsm32::smem, st>>>(
+            L, factors, nullptr, 0, 0, 0, a, 0, nullptr, 0);
+      } else {
+        gemm_attr<2, GTrsm>();
+        large_update_kernel<2, GTrsm><<<g, GTrsm::NT, GTrsm::smem, st>>>(L, factors, nullptr, 0, 0,
+                                                                     0, a, 0, nullptr, 0);
+      }
       timer_end(st);
     }
     return cudaGetLastError();
