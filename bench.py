@@ -254,17 +254,23 @@ def run_ours(args, cfg):
     x_host = torch.empty((n, nrhs), dtype=torch.float64).pin_memory()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     elem_host = torch.from_numpy(np.ascontiguousarray(fronts.values).ravel()).pin_memory()
+    copy_stream = torch.cuda.Stream(dev)
+    b_dev = torch.empty((n, nrhs), dtype=torch.float64, device=dev)
+
     def e2e_step():
         dp.elem.copy_(elem_host, non_blocking=True)               # H2D: element matrices
+        with torch.cuda.stream(copy_stream):                      # H2D: right-hand sides,
+            b_dev.copy_(b_host, non_blocking=True)                # overlapping the factorization
         if sharded is not None:                                   # sharded path (N > 1)
-            bd = b_host.to(dev, non_blocking=True)                # H2D: right-hand sides
             if sharded.factor(thr, stream) != -1:
                 raise RuntimeError("zero pivot")
-            xd = torch.empty_like(bd)
-            sharded.solve_into(bd, xd, stream)
+            stream.wait_stream(copy_stream)
+            xd = torch.empty_like(b_dev)
+            sharded.solve_into(b_dev, xd, stream)
         else:
             fac = tf.run_sequential(plan, state)                  # public API (checks pivots)
-            xd = tf.solve(fac, b_host.to(dev, non_blocking=True))  # H2D: right-hand sides
+            stream.wait_stream(copy_stream)
+            xd = tf.solve(fac, b_dev)
         x_host.copy_(xd, non_blocking=True)                       # D2H: solution
         torch.cuda.synchronize()
 
