@@ -17,6 +17,9 @@
 //                 Y_b = M W_b then W_rows -= L_rows,b Y_b (one launch per
 //                 block); backward X_b = M^T (X_b - sum_rows L_rows,b^T X_rows)
 //                 with a deterministic two-pass reduction over row chunks.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace tfb {
@@ -685,12 +688,30 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
 #define TFB_SMALL(G, GPC)                                                                    \
   launch_small_solve<G, GPC, FWD, false>(L, O, flag, factors, w_in, in_rows, w_out, out_rows, \
                                          y, nr, nrhs, col0, st)
-      if (work <= 12) e = TFB_SMALL(1, 128);
-      else if (work <= 24) e = TFB_SMALL(2, 64);
-      else if (work <= 48) e = TFB_SMALL(4, 64);
-      else if (work <= 96) e = TFB_SMALL(8, 32);
-      else if (work <= 256) e = TFB_SMALL(32, 8);
-      else e = TFB_SMALL(128, 2);
+      // (G, GPC) per class m <= 12, 24, 48, 96, 256, rest; TFB_SOLVE_CFG overrides
+      static int cfg[6][2] = {{1, 128}, {2, 64}, {4, 64}, {8, 32}, {32, 8}, {128, 2}};
+      static bool parsed = false;
+      if (!parsed) {
+        parsed = true;
+        if (const char* ev = getenv("TFB_SOLVE_CFG")) {
+          for (int i = 0; i < 6 && *ev; i++) {
+            int g = 0, n = 0;
+            if (sscanf(ev, "%d:%d", &g, &n) == 2) { cfg[i][0] = g; cfg[i][1] = n; }
+            while (*ev && *ev != ',') ev++;
+            if (*ev == ',') ev++;
+          }
+        }
+      }
+      const int cls = work <= 12 ? 0 : work <= 24 ? 1 : work <= 48 ? 2 : work <= 96 ? 3
+                    : work <= 256 ? 4 : 5;
+      const int G = cfg[cls][0], GPC = cfg[cls][1];
+      e = cudaErrorInvalidValue;
+#define TFB_CASE(g, n) \
+  if (G == g && GPC == n) e = TFB_SMALL(g, n);
+      TFB_CASE(1, 128) TFB_CASE(1, 256) TFB_CASE(1, 64) TFB_CASE(2, 64) TFB_CASE(2, 128)
+      TFB_CASE(4, 64) TFB_CASE(4, 32) TFB_CASE(8, 32) TFB_CASE(8, 16) TFB_CASE(16, 16)
+      TFB_CASE(16, 8) TFB_CASE(32, 8) TFB_CASE(32, 4) TFB_CASE(64, 4) TFB_CASE(128, 2)
+#undef TFB_CASE
 #undef TFB_SMALL
     } else {
       const long long bytes = (work + (long long)L.max_m * L.max_k + L.max_m) * 8;
