@@ -66,13 +66,26 @@ __global__ void __launch_bounds__(32 * kAsmWarps)
     const int i1 = two ? inv1[r] : -1, t1 = i1 >= 0 ? tri32(i1, 0) : 0;
     double* prow = Pf + (long long)r * kp;
     const int pc = min(r + 1, k);
-    for (int c = lane; c < kp; c += 32) {
+    if (kp <= 32) {  // narrow panels: one column per lane
       double v = 0.0;
-      if (c < pc) {
-        v = child_entry(src0, i0, t0, inv0[c]);
-        if (two) v += child_entry(src1, i1, t1, inv1[c]);
+      if (lane < pc) v = child_entry(src0, i0, t0, inv0[lane]) + child_entry(src1, i1, t1, two ? inv1[lane] : -1);
+      if (lane < kp) prow[lane] = v;
+    } else
+    for (int c0 = lane; c0 < kp; c0 += 128) {  // 4 columns per lane in flight
+      int j0[4], j1[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int c = c0 + 32 * q;
+        j0[q] = c < pc ? inv0[c] : -1;
+        j1[q] = (two && c < pc) ? inv1[c] : -1;
       }
-      prow[c] = v;
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        v[q] = child_entry(src0, i0, t0, j0[q]) + child_entry(src1, i1, t1, j1[q]);
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (c0 + 32 * q < kp) prow[c0 + 32 * q] = v[q];
     }
     if (with_s && r >= k) {  // else the Schur kernel assembles S in its epilogue
       const int a = r - k;
