@@ -85,7 +85,19 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
       }
     } else {
       const double* src = c == 0 ? src0 : src1;
-      for (int e = t; e < n; e += G) F[__ldg(scc + e)] += src[e];
+      int e = t;
+      for (; e + 3 * G < n; e += 4 * G) {  // four entries per thread in flight
+        int p[4];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          p[q] = __ldg(scc + e + q * G);
+          v[q] = src[e + q * G];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) F[p[q]] += v[q];
+      }
+      for (; e < n; e += G) F[__ldg(scc + e)] += src[e];
     }
     group_sync<G>(bar);
   }
