@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(G* GPC)
                     double* w_out, long long out_rows, double* y, int nr, int ldr, int col0,
                     int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
   if (f >= L.n_fronts) return;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(G* GPC)
                     long long out_rows, double* y, int nr, int ldr, int col0,
                     int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
   if (f >= L.n_fronts) return;
