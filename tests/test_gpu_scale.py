@@ -26,7 +26,7 @@ def limit(request, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shape,p", [((256, 256), 1), ((512, 512), 1), ((128, 128), 2), ((16, 16, 16), 1),
+@pytest.mark.parametrize("shape,p", [((256, 256), 1), ((512, 512), 1), ((1024, 1024), 1), ((128, 128), 2), ((16, 16, 16), 1),
                                      ((40, 24), 3)])
 def test_residual_at_scale(shape, p, limit):
     mesh, fronts, system, plan = pipeline(shape, p)
