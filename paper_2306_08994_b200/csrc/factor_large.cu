@@ -715,31 +715,45 @@ __global__ void __launch_bounds__(G::NT, 4) large_update_kernel(LevelArgs L, dou
     const bool two = s.nsrc == 2;
     const double* src0 = child_upd + L.child_slot(f, 0) * L.child_upd_stride;
     const double* src1 = child_upd + L.child_slot(f, 1) * L.child_upd_stride;
+    // column maps once per thread, then per row: all child loads issued
+    // before any store (no branches between them)
+    int b0[NJ][2], b1[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int cl = wx * G::WN + j * 8 + 2 * (lane & 3) + h;
+        const bool ok = cl < nB;
+        b0[j][h] = ok ? __ldg(inv0 + k + (int)tile_c0 + cl) : -1;
+        b1[j][h] = (ok && two) ? __ldg(inv1 + k + (int)tile_c0 + cl) : -1;
+      }
 #pragma unroll
     for (int i = 0; i < MI; i++) {
       const int rl = wy * G::WM + i * 8 + (lane >> 2);
-      if (rl >= nA) continue;
+      const bool okr = rl < nA;
       const int R = (int)tile_r0 + rl;
-      const int a0 = inv0[k + R], ta0 = a0 >= 0 ? tri32(a0, 0) : 0;
-      const int a1 = two ? inv1[k + R] : -1, ta1 = a1 >= 0 ? tri32(a1, 0) : 0;
+      const int a0 = okr ? __ldg(inv0 + k + R) : -1, ta0 = a0 >= 0 ? tri32(a0, 0) : 0;
+      const int a1 = (okr && two) ? __ldg(inv1 + k + R) : -1, ta1 = a1 >= 0 ? tri32(a1, 0) : 0;
+      double v[NJ][2];
+#pragma unroll
+      for (int j = 0; j < NJ; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int c0 = b0[j][h], c1 = b1[j][h];
+          const double x0 = (a0 >= 0 && c0 >= 0) ? __ldg(src0 + (a0 >= c0 ? ta0 + c0 : tri32(c0, a0))) : 0.0;
+          const double x1 = (a1 >= 0 && c1 >= 0) ? __ldg(src1 + (a1 >= c1 ? ta1 + c1 : tri32(c1, a1))) : 0.0;
+          v[j][h] = x0 + x1;
+        }
+      if (!okr) continue;
       double* orow = out + tri32(R, 0);
 #pragma unroll
-      for (int j = 0; j < NJ; j++) {
+      for (int j = 0; j < NJ; j++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int cl = wx * G::WN + j * 8 + 2 * (lane & 3) + h;
           const int C = (int)tile_c0 + cl;
-          if (cl >= nB || C > R) continue;
-          double v = 0.0;
-          const int b0 = inv0[k + C];
-          if (a0 >= 0 && b0 >= 0) v = src0[a0 >= b0 ? ta0 + b0 : tri32(b0, a0)];
-          if (two) {
-            const int b1 = inv1[k + C];
-            if (a1 >= 0 && b1 >= 0) v += src1[a1 >= b1 ? ta1 + b1 : tri32(b1, a1)];
-          }
-          orow[C] = v - acc[i][j][h];
+          if (cl < nB && C <= R) orow[C] = v[j][h] - acc[i][j][h];
         }
-      }
     }
     return;
   }
