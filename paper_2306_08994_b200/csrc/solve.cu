@@ -109,7 +109,20 @@ __global__ void __launch_bounds__(G* GPC)
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
       const double* Wc = w_child + (ch * child_rows + off) * ldr + col0;
       const int n = len * nr;
-      for (int e = t; e < n; e += G) {
+      int e = t;
+      for (; e + 3 * G < n; e += 4 * G) {  // four entries in flight per thread
+        int p[4];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int eq = e + q * G, a = eq / nr, j = eq - a * nr;
+          p[q] = __ldg(mp + a) * nr + j;
+          v[q] = Wc[(long long)a * ldr + j];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) W[p[q]] += v[q];
+      }
+      for (; e < n; e += G) {
         const int a = e / nr, j = e - a * nr;
         W[mp[a] * nr + j] += Wc[(long long)a * ldr + j];
       }
@@ -173,7 +186,18 @@ __global__ void __launch_bounds__(G* GPC)
     const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
     const int* mp = PA.maps + (c == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
     const double* Xp = x_parent + pf * parent_rows * ldr + col0;
-    for (int e = nK + t; e < nW; e += G) {
+    int e = nK + t;
+    for (; e + 3 * G < nW; e += 4 * G) {  // four entries in flight per thread
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int eq = e + q * G - nK, a = eq / nr, j = eq - a * nr;
+        v[q] = Xp[(long long)__ldg(mp + a) * ldr + j];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) X[e + q * G] = v[q];
+    }
+    for (; e < nW; e += G) {
       const int a = (e - nK) / nr, j = (e - nK) % nr;
       X[e] = Xp[(long long)mp[a] * ldr + j];
     }
