@@ -102,6 +102,47 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
     group_sync<G>(bar);
   }
 
+  // (2) panel.  Wide groups (G >= 128, the larger fronts) with k >= 16:
+  // (a) the k x k pivot block, right-looking with unscaled columns (one
+  // barrier per pivot), scaled to l; (b) every L21 row independently (no
+  // barriers): forward substitution against L11, u_rc = a_rc - sum_{q<c}
+  // u_rq l(c,q), then l(r,c) = u_rc / d_c.
+  if constexpr (G >= 128) {
+    if (k >= 16) {
+      const long long piv0 = L.piv_off[f];
+      for (int c = 0; c < k; c++) {
+        const double d = F[tri32(c, c)];
+        if (t == 0 && fabs(d) <= threshold) record_zero_pivot(err, (unsigned long long)(piv0 + c));
+        const double dinv = 1.0 / d;
+        for (int r = c + 1 + t; r < k; r += G) {
+          double* row = F + tri32(r, 0);
+          const double lrc = row[c] * dinv;
+          for (int q = c + 1; q <= r; q++) row[q] -= lrc * F[tri32(q, c)];
+        }
+        group_sync<G>(bar);
+      }
+      for (int c = t; c < k; c += G) lv[c] = 1.0 / F[tri32(c, c)];
+      group_sync<G>(bar);
+      for (int r = 1 + t; r < k; r += G) {
+        double* row = F + tri32(r, 0);
+        for (int c = 0; c < r; c++) row[c] *= lv[c];
+      }
+      group_sync<G>(bar);
+      for (int r = k + t; r < m; r += G) {
+        double* row = F + rowp(r);
+        for (int c = 1; c < k; c++) {
+          const double* lc = F + tri32(c, 0);
+          double u = row[c];
+          for (int q = 0; q < c; q++) u -= row[q] * lc[q];
+          row[c] = u;
+        }
+        for (int c = 0; c < k; c++) row[c] *= lv[c];
+      }
+      group_sync<G>(bar);
+      goto schur;
+    }
+  }
+  {
   // (2) panel: right-looking over the k pivot columns, updates confined to
   // them, columns kept unscaled during the sweep (a(r,q) -= a(r,c) a(q,c) / d_c
   // reads only finished column-c entries: one barrier per pivot), then scaled.
@@ -129,6 +170,8 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
     group_sync<G>(bar);
   }
 
+  }
+schur:
   // (3) Schur block: S[i][j] -= sum_q L21[i][q] d_q L21[j][q], i >= j
   if (k > 0 && u > 0) {
     for (int c = t; c < k; c += G) lv[c] = F[tri32(c, c)];  // pivots
