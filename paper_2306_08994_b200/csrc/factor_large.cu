@@ -915,6 +915,15 @@ static LookaheadStreams& lookahead_streams() {
   return ls;
 }
 
+static int schur_group() {  // TFB_SCHUR_GROUP (tuning)
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TFB_SCHUR_GROUP");
+    v = e ? std::max(1, atoi(e)) : 1;
+  }
+  return v;
+}
+
 static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd, double* factors,
                                     double* upd_out,
                                     double thr, unsigned long long* err, cudaStream_t st) {
@@ -942,11 +951,14 @@ static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd,
       launch_panel_update(L, factors, c2, L.max_k, c0, c1, S.panel);
       cudaEventRecord(S.panel_done, S.panel);
     }
-    if (schur) {
+    // Schur chunks cover schur_group() super-blocks (fewer read-modify-write
+    // passes over S); the first chunk also assembles S (children gathered in
+    // its epilogue)
+    if (schur && ((j + 1) % schur_group() == 0 || j + 1 == nsb)) {
+      const int g0 = (j / schur_group()) * schur_group() * W;
       cudaStreamWaitEvent(S.schur, S.chain_done, 0);
       timer_begin(K_SCHUR, S.schur);
-      // the first chunk also assembles S (children gathered in its epilogue)
-      launch_schur<GSchurA>(L, factors, upd_out, S.schur, c0, c1, j == 0 ? child_upd : nullptr);
+      launch_schur<GSchurA>(L, factors, upd_out, S.schur, g0, c1, g0 == 0 ? child_upd : nullptr);
       timer_end(S.schur);
     }
   }
@@ -1039,7 +1051,8 @@ int large_level_launches(int max_k, int max_upd, long long level_fronts) {
     int n = 2;  // assembly, finalize
     for (int j = 0; j < nsb; j++) {
       const int c0 = j * W, c1 = std::min(c0 + W, max_k);
-      n += large_panel_launches(c1 - c0, fronts) + (j + 1 < nsb) + (j + 2 < nsb) + (max_upd > 0);
+      n += large_panel_launches(c1 - c0, fronts) + (j + 1 < nsb) + (j + 2 < nsb) +
+           (max_upd > 0 && ((j + 1) % schur_group() == 0 || j + 1 == nsb));
     }
     return n;
   }
