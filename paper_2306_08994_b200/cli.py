@@ -18,6 +18,8 @@ from typing import Optional
 
 import numpy as np
 
+from . import fileio
+
 EXIT_OK, EXIT_USAGE, EXIT_NUMERICAL, EXIT_VERIFY = 0, 1, 2, 3
 DEFAULT_ORACLE_CAP = 2000
 
@@ -44,6 +46,7 @@ def build_parser() -> _Parser:
         p.add_argument("--nrhs", type=int, default=1)
         p.add_argument("--out", type=Path, default=Path("."))
 
+    common(sub.add_parser("generate", help="export matrix.mtx, rhs.txt, manifest.json"))
     common(sub.add_parser("plan", help="tree / level-schedule statistics"))
     common(sub.add_parser("factorize", help="factorize and export the pivot order"))
     common(sub.add_parser("solve", help="factorize and solve, export the solution"))
@@ -92,6 +95,26 @@ def _rhs(system, nrhs):
     return np.concatenate([b[:, None], extra], axis=1)
 
 
+def cmd_generate(args, parser) -> int:
+    """matrix.mtx, rhs.txt, manifest.json (cli.py:164-183)."""
+    import json
+    mesh = _mesh(args, parser)
+    from .fem import assemble_system
+    system = assemble_system(mesh, args.rhs)
+    args.out.mkdir(parents=True, exist_ok=True)
+    fileio.write_matrix_market_symmetric(args.out / "matrix.mtx", system)
+    fileio.write_vector(args.out / "rhs.txt", system.rhs)
+    manifest = {"n_elements": int(getattr(mesh, "n_elements", 0)), "degree": mesh.degree,
+                "n_dof": mesh.n_dof, "rhs": args.rhs}
+    if hasattr(mesh, "domain_start"):
+        manifest["domain"] = [mesh.domain_start, mesh.domain_end]
+    if hasattr(mesh, "shape"):
+        manifest["shape"] = list(mesh.shape)
+    (args.out / "manifest.json").write_text(json.dumps(manifest, sort_keys=True, indent=2) + "\n")
+    print(f"wrote matrix.mtx rhs.txt manifest.json to {args.out} (n_dof={mesh.n_dof})")
+    return EXIT_OK
+
+
 def cmd_plan(args, parser) -> int:
     mesh = _mesh(args, parser)
     tf, system, tree, plan = _pipeline(mesh, args.rhs)
@@ -125,12 +148,18 @@ def cmd_factorize_solve(args, parser) -> int:
     tf, system, tree, plan = _pipeline(mesh, args.rhs)
     factors, wall = _factorize(tf, plan, system)
     args.out.mkdir(parents=True, exist_ok=True)
-    if args.command == "factorize":
-        np.savetxt(args.out / "pivot_order.txt", plan.pivot_order_array, fmt="%d")
+    if args.command == "factorize":  # cli.py:207-218 exports
+        lower, upper = fileio.factor_exports(factors)
+        fileio.write_matrix_market_general(args.out / "L.mtx", mesh.n_dof, mesh.n_dof, lower)
+        fileio.write_matrix_market_general(args.out / "U.mtx", mesh.n_dof, mesh.n_dof, upper)
+        fileio.write_vector(args.out / "pivot_order.txt", factors.pivot_order)
     else:
         b = _rhs(system, args.nrhs)
         x = tf.solve(factors, b)
-        np.savetxt(args.out / "solution.txt", x, fmt="%r" if x.ndim == 1 else "%.17g")
+        if x.ndim == 1:
+            fileio.write_vector(args.out / "solution.txt", x)
+        else:
+            np.savetxt(args.out / "solution.txt", x, fmt="%.17g")
         r = system.matvec(x) - b
         scale = np.linalg.norm(b)
         print(f"residual={np.linalg.norm(r) / (scale if scale > 0 else 1.0):.3e}")
@@ -205,7 +234,7 @@ def main(argv: Optional[list[str]] = None) -> int:
     from .errors import TracefrontError, ZeroPivotError
     parser = build_parser()
     args = parser.parse_args(argv)
-    cmds = {"plan": cmd_plan, "factorize": cmd_factorize_solve, "solve": cmd_factorize_solve,
+    cmds = {"generate": cmd_generate, "plan": cmd_plan, "factorize": cmd_factorize_solve, "solve": cmd_factorize_solve,
             "verify": cmd_verify, "bench": cmd_bench}
     try:
         return cmds[args.command](args, parser)
