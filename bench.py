@@ -309,10 +309,23 @@ def run_ours(args, cfg):
             asm_bytes += st["bytes"] - 8.0 * st["upd_entries"]
         else:
             small_bytes += st["bytes"]
+    # solve sweeps (per direction): factor entries read once + the front
+    # vector blocks written and read (8 B x nrhs per front row, twice)
+    solve_small = solve_large = 0.0
+    for L, (dl, st) in enumerate(zip(dp.levels, stats)):
+        b_ = 8.0 * st["fac_entries"] + 16.0 * nrhs * float(dl.tables.front_m().sum())
+        if large[L]:
+            solve_large += b_
+        else:
+            solve_small += b_
     work = {  # algorithmic work per step of each kernel class
         "large_update_kernel<1> (schur)": ("tensor", schur_flops),
         "factor_small_kernel": ("hbm", small_bytes),
         "large_assemble_kernel": ("hbm", asm_bytes),
+        "solve_fwd_small": ("hbm", solve_small),
+        "solve_bwd_small": ("hbm", solve_small),
+        "solve_fwd_wave": ("hbm", solve_large),
+        "solve_bwd_wave": ("hbm", solve_large),
     }
     name = max(ktime, key=lambda k: ktime[k][0])
     tot_ms = sum(v[0] for v in ktime.values())
