@@ -21,8 +21,8 @@ inline bool level_is_large(int is_leaf, int max_m) { return !is_leaf && max_m > 
 // Kernel classes for the optional launch timing (timing.cu).
 enum KernelClass {
   K_SMALL = 0, K_SUBTREE, K_ASSEMBLE, K_DIAG, K_BLOCK, K_TRSM, K_PANEL, K_SCHUR, K_FINALIZE,
-  K_SOLVE_SMALL_FWD, K_SOLVE_SMALL_BWD, K_SOLVE_GATHER, K_SOLVE_FWD_BLOCK, K_SOLVE_BWD_PARTIAL,
-  K_SOLVE_BWD_BLOCK, K_PERMUTE, K_COUNT
+  K_SOLVE_SMALL_FWD, K_SOLVE_SMALL_BWD, K_SOLVE_GATHER, K_SOLVE_FWD_WAVE, K_SOLVE_BWD_WAVE,
+  K_PERMUTE, K_COUNT
 };
 void timer_begin(int cls, cudaStream_t st);
 void timer_end(cudaStream_t st);

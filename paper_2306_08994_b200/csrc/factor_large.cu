@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(G::NT, 4) large_update_kernel(LevelArgs L, dou
   }
 }
 
-// Tile shapes measured on B200 (tools/schur_sweep.sh): 64x64 tiles of 8 warps
+// Tile shapes measured on B200 (A/B builds via TFB_LIB): 64x64 tiles of 8 warps
 // with a 2-stage pipeline keep the most warps resident and win on every level.
 using GTrsm = GemmCfg<64, 64, 16, 2>;   // N = 64 = one diagonal block
 using GTrsm32 = GemmCfg<64, 32, 16, 2, 4, 1>;  // blocks of <= 32 columns: 4 warps of 16x32

@@ -807,7 +807,7 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
     const int nbuf = L.n_fronts <= kWaveFewFronts ? 3 : 1;
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
     if (nb > 0) cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb, st);
-    timer_begin(K_SOLVE_FWD_BLOCK, st);
+    timer_begin(K_SOLVE_FWD_WAVE, st);
     if (nr == 1) {
       const unsigned g = wave_grid(solve_fwd_wave<true>, smem, (long long)rt * L.n_fronts);
       solve_fwd_wave<true><<<g, 256, smem, st>>>(L, C, child_at0, factors, w_child, child_rows,
@@ -850,7 +850,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
     const int nbuf = L.n_fronts <= kWaveFewFronts ? 2 : 1;
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr + 4 * TB);
     cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb * (1 + rt), st);
-    timer_begin(K_SOLVE_BWD_BLOCK, st);
+    timer_begin(K_SOLVE_BWD_WAVE, st);
     if (nr == 1) {
       const unsigned g = wave_grid(solve_bwd_wave<true>, smem, ntiles);
       solve_bwd_wave<true><<<g, 256, smem, st>>>(L, factors, x_out, out_rows, y, nr, nrhs, col0,
