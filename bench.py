@@ -202,6 +202,9 @@ def run_ours(args, cfg):
     if world > 1:
         from paper_2306_08994_b200.distributed import ShardedFactorization, TorchComm
         sharded = ShardedFactorization(dp, world, TorchComm(), ranks=[rank])
+        # a collective on every rank before the first (partial) P2P batch, so
+        # the NCCL communicator exists on all ranks
+        dist.barrier()
 
     def step(ev=None):
         record = ev is not None
