@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(G* GPC)
   double* W = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
+  if (L.is_leaf && k == 0) return;  // element without pivots: its update block is 0 (memset)
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(G* GPC)
   double* X = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
+  if (L.is_leaf && k == 0) return;  // nothing to solve and no children to serve
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -706,6 +708,10 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
                                   double* w_out, long long out_rows, double* y, int nrhs,
                                   cudaStream_t st) {
   const int cw = small_cols(L, nrhs);
+  if (FWD && L.is_leaf) {  // fronts without pivots leave zero update blocks
+    cudaError_t e = cudaMemsetAsync(w_out, 0, sizeof(double) * (size_t)L.n_fronts * out_rows * nrhs, st);
+    if (e != cudaSuccess) return e;
+  }
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
     const long long work = (long long)L.max_m * nr;
