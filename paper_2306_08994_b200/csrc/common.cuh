@@ -22,7 +22,7 @@ inline bool level_is_large(int is_leaf, int max_m) { return !is_leaf && max_m > 
 enum KernelClass {
   K_SMALL = 0, K_SUBTREE, K_ASSEMBLE, K_DIAG, K_BLOCK, K_TRSM, K_PANEL, K_SCHUR, K_FINALIZE,
   K_SOLVE_SMALL_FWD, K_SOLVE_SMALL_BWD, K_SOLVE_GATHER, K_SOLVE_FWD_WAVE, K_SOLVE_BWD_WAVE,
-  K_PERMUTE, K_COUNT
+  K_PERMUTE, K_ROOT, K_COUNT
 };
 void timer_begin(int cls, cudaStream_t st);
 void timer_end(cudaStream_t st);
@@ -165,6 +165,15 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace tfb

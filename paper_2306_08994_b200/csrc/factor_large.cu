@@ -13,7 +13,9 @@
 //   3. one DMMA update S -= L21 D L21^T over all k pivots.
 // Arithmetic replaced: engine.py:86-105 per pivot (Division, Multiplication,
 // Subtraction) and engine.py:537-545 (factorize_nested_loops inner loops).
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -975,6 +977,279 @@ static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd,
   return cudaGetLastError();
 }
 
+static bool root_dataflow() {  // TFB_ROOT_DATAFLOW=0 selects the lookahead path (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_ROOT_DATAFLOW");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
+// ------------------------------------------------------------- root fronts
+// Fronts without a Schur block (the root, m == k): one persistent launch that
+// factors the whole front as a dataflow over its 64x64 lower tiles (i, l),
+// left-looking.  Tiles are dealt in column-major order from an atomic
+// counter, so a tile only waits on tiles dealt before it to running CTAs (no
+// deadlock, whatever the residency).  Tile (i, l) accumulates
+// sum_{j<l} L_ij D_j L_lj^T as the columns j are published (flags,
+// acquire/release), subtracts it from its assembled value, then either
+// factors it (i == l: diag64_smem, l and d into the panel, aux block) or
+// solves it (i > l: L_il = A M_l^T D_l^-1) and publishes it.  The pivot chain
+// is one diagonal factorization + one tile solve + one 64-deep product per
+// column, with no launch gaps; sums run in a fixed order (deterministic).
+using GRoot = GemmCfg<64, 64, 16, 2>;
+constexpr size_t kRootSmem = sizeof(double) * (2 * NB * DLD + NB);
+static_assert(GRoot::smem <= kRootSmem, "GEMM staging fits the diagonal-block buffers");
+
+__device__ __forceinline__ void root_wait(const int* flag) {
+  while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+}
+
+__global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double* factors,
+                                                         double threshold,
+                                                         unsigned long long* err, int* flags,
+                                                         int T, long long* trace) {
+  constexpr int BK = GRoot::BK, ST = GRoot::ST, LD = GRoot::LD, MI = GRoot::MI, NJ = GRoot::NJ;
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ int s_tile;
+  double* As = rsm;                 // GEMM staging [ST][64][LD], [ST][64][LD], [ST][BK]
+  double* Bs = As + ST * NB * LD;
+  double* Ds = Bs + ST * NB * LD;
+  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm);             // tile / diagonal block
+  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + NB * DLD);  // inverse block
+  double* dv = rsm + 2 * NB * DLD;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
+  const long long per_front = (long long)T * (T + 1) / 2;
+  const long long ntiles = per_front * L.n_fronts;
+  int* counter = flags + (long long)L.n_fronts * T * T;
+  for (;;) {
+    __syncthreads();  // shared memory is reused tile to tile
+    if (tid == 0) s_tile = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long t = s_tile;
+    if (t >= ntiles) return;
+    const long long f = t % L.n_fronts;
+    long long rr = t / L.n_fronts;
+    int l = 0;
+    while (rr >= T - l) rr -= T - l++;
+    const int i = l + (int)rr;
+    const Shape s = front_shape(L, f);
+    const int k = s.k, kp = s.kp;
+    const int r0 = i * NB, c0 = l * NB;
+    if (r0 >= k) continue;  // beyond this front (smaller than the level's largest)
+    const int nA = min(NB, k - r0), nB = min(NB, k - c0);
+    double* Pf = factors + f * L.fac_stride;
+    double* dvec = Pf + (long long)s.m * kp;
+    int* fl = flags + f * T * T;
+    const int nk = l * (NB / BK);
+
+    auto issue = [&](int it) {
+      const int stage = it % ST, kt = it * BK;
+      double* as = As + stage * NB * LD;
+      double* bs = Bs + stage * NB * LD;
+      constexpr int CPR = BK / 2;
+#pragma unroll
+      for (int q = 0; q < (NB * CPR) / 256; q++) {
+        const int ch = tid + q * 256, r = ch / CPR, cc = (ch % CPR) * 2;
+        const bool va = r < nA, vb = r < nB;
+        cp_async16(as + r * LD + cc, va ? Pf + (long long)(r0 + r) * kp + kt + cc : Pf, va);
+        cp_async16(bs + r * LD + cc, vb ? Pf + (long long)(c0 + r) * kp + kt + cc : Pf, vb);
+      }
+      if (tid < CPR) cp_async16(Ds + stage * BK + tid * 2, dvec + kt + tid * 2, true);
+    };
+    // column j of the product is ready once tiles (i, j) and (l, j) are published
+    auto wait_col = [&](int it) {
+      if (tid == 0 && (it % (NB / BK)) == 0) {
+        const int j = it / (NB / BK);
+        root_wait(fl + i * T + j);
+        if (i != l) root_wait(fl + l * T + j);
+      }
+    };
+
+    double acc[MI][NJ][2];
+#pragma unroll
+    for (int a = 0; a < MI; a++)
+#pragma unroll
+      for (int b = 0; b < NJ; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    if (nk > 0) {
+      wait_col(0);
+      __syncthreads();
+      issue(0);
+    }
+    cp_async_commit();
+    for (int it = 0; it < nk; it++) {
+      if (it + 1 < nk) wait_col(it + 1);
+      cp_async_wait<0>();
+      __syncthreads();
+      if (it + 1 < nk) issue(it + 1);
+      cp_async_commit();
+      const int stage = it % ST;
+      const double* as = As + stage * NB * LD + (wy * GRoot::WM + g8) * LD + tq;
+      const double* bs = Bs + stage * NB * LD + (wx * GRoot::WN + g8) * LD + tq;
+      const double* ds = Ds + stage * BK + tq;
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        const double dk = ds[ks];
+        double af[MI], bf[NJ];
+#pragma unroll
+        for (int a = 0; a < MI; a++) af[a] = as[a * 8 * LD + ks] * dk;
+#pragma unroll
+        for (int b = 0; b < NJ; b++) bf[b] = bs[b * 8 * LD + ks];
+#pragma unroll
+        for (int a = 0; a < MI; a++)
+#pragma unroll
+          for (int b = 0; b < NJ; b++) dmma884(acc[a][b], af[a], bf[b]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // staging buffers become D / Mi
+    auto stamp = [&](int slot) {
+      if (trace && tid == 0 && f == 0 && (i == l || i == l + 1)) {
+        long long ns;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ns));
+        trace[(long long)l * 8 + (i == l ? 0 : 4) + slot] = ns;
+      }
+    };
+    stamp(0);
+
+    // A = assembled tile - accumulated product, into D (unit rows/zeros outside)
+#pragma unroll
+    for (int a = 0; a < MI; a++) {
+      const int rl = wy * GRoot::WM + a * 8 + g8;
+#pragma unroll
+      for (int b = 0; b < NJ; b++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+          const bool in = rl < nA && cl < nB && (i != l || cl <= rl);
+          D[rl][cl] = in ? Pf[(long long)(r0 + rl) * kp + c0 + cl] - acc[a][b][h]
+                         : (rl == cl ? 1.0 : 0.0);
+        }
+    }
+    if (i == l) {
+      __syncthreads();
+      diag64_smem<256>(D, Mi, dv, nB);
+      stamp(1);
+      for (int e = tid; e < NB * NB; e += 256) {
+        const int a = e >> 6, b = e & 63;
+        if (a < nB && b <= a) Pf[(long long)(r0 + a) * kp + c0 + b] = D[a][b];
+      }
+      for (int c = tid; c < nB; c += 256) {
+        dvec[c0 + c] = dv[c];
+        if (fabs(dv[c]) <= threshold)
+          record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + c0 + c));
+      }
+      write_aux64<256>(L.aux + f * L.aux_stride + (long long)l * NB * NB, D, Mi, dv, nB);
+    } else {
+      // L_il = A M_l^T D_l^-1 (M_l: strict lower part of the aux block)
+      if (tid == 0) root_wait(fl + l * T + l);
+      stamp(1);
+      __syncthreads();
+      const double* M = L.aux + f * L.aux_stride + (long long)l * NB * NB;
+      for (int e = tid; e < NB * NB; e += 256) {
+        const int a = e >> 6, b = e & 63;
+        Mi[a][b] = b < a ? M[e] : (b == a ? 1.0 : 0.0);
+      }
+      if (tid < NB) dv[tid] = tid < nB ? dvec[c0 + tid] : 1.0;
+      __syncthreads();
+      double x[MI][NJ][2];
+#pragma unroll
+      for (int a = 0; a < MI; a++)
+#pragma unroll
+        for (int b = 0; b < NJ; b++) x[a][b][0] = x[a][b][1] = 0.0;
+#pragma unroll 4
+      for (int ks = 0; ks < NB; ks += 4) {
+        double af[MI], bf[NJ];
+#pragma unroll
+        for (int a = 0; a < MI; a++) af[a] = D[wy * GRoot::WM + a * 8 + g8][ks + tq];
+#pragma unroll
+        for (int b = 0; b < NJ; b++) bf[b] = Mi[wx * GRoot::WN + b * 8 + g8][ks + tq];
+#pragma unroll
+        for (int a = 0; a < MI; a++)
+#pragma unroll
+          for (int b = 0; b < NJ; b++) dmma884(x[a][b], af[a], bf[b]);
+      }
+#pragma unroll
+      for (int a = 0; a < MI; a++) {
+        const int rl = wy * GRoot::WM + a * 8 + g8;
+#pragma unroll
+        for (int b = 0; b < NJ; b++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+            if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] / dv[cl];
+          }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_gpu(fl + i * T + l, 1);
+    }
+    stamp(2);
+  }
+}
+
+static int* root_flags(long long ints) {  // per-device scratch, grown on demand
+  static int* buf[64] = {};
+  static long long cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (cap[dev] < ints) {
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&buf[dev], sizeof(int) * ints) != cudaSuccess) return nullptr;
+    cap[dev] = ints;
+  }
+  return buf[dev];
+}
+
+static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
+                               unsigned long long* err, cudaStream_t st) {
+  const int T = (L.max_k + NB - 1) / NB;
+  const long long nflags = (long long)L.n_fronts * T * T + 1;
+  int* flags = root_flags(nflags);
+  if (!flags) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * nflags, st);
+  if (e != cudaSuccess) return e;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(large_root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kRootSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, large_root_kernel, 256, kRootSmem);
+    occ = std::max(occ, 1);
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long ntiles = (long long)L.n_fronts * T * (T + 1) / 2;
+  const unsigned grid = (unsigned)std::max(1LL, std::min(ntiles, (long long)sms * occ));
+  timer_begin(K_ROOT, st);
+  static long long* trace = nullptr;
+  if (getenv("TFB_ROOT_TRACE") && !trace) {
+    cudaMalloc(&trace, sizeof(long long) * 8 * 4096);
+    cudaMemset(trace, 0, sizeof(long long) * 8 * 4096);
+  }
+  large_root_kernel<<<grid, 256, kRootSmem, st>>>(L, factors, thr, err, flags, T, trace);
+  if (trace && T <= 4096) {
+    static std::vector<long long> h;
+    h.resize(8 * T);
+    cudaMemcpyAsync(h.data(), trace, sizeof(long long) * 8 * T, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const long long t0 = h[0];
+    for (int l = 0; l < T; l++)
+      fprintf(stderr, "col %3d diag: ready %8.1f done %8.1f pub %8.1f | trsm: ready %8.1f pub %8.1f us\n", l,
+              (h[8 * l] - t0) * 1e-3, (h[8 * l + 1] - t0) * 1e-3, (h[8 * l + 2] - t0) * 1e-3,
+              (h[8 * l + 5] - t0) * 1e-3, (h[8 * l + 6] - t0) * 1e-3);
+  }
+  timer_end(st);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, double* factors,
                                 double* upd_out, double thr, unsigned long long* err,
                                 cudaStream_t st) {
@@ -1008,6 +1283,8 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (L.max_upd == 0 && L.max_k > 0 && root_dataflow())
+    return factor_root(L, factors, thr, err, st);
   if (lookahead) return factor_lookahead(L, child_upd, factors, upd_out, thr, err, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);
@@ -1045,6 +1322,7 @@ int large_panel_launches(int max_k, int n_fronts) {
 // Kernel launches of one launch_factor_large call (tf_level_launch_count).
 int large_level_launches(int max_k, int max_upd, long long level_fronts) {
   const int fronts = (int)std::min<long long>(level_fronts, 1 << 30);
+  if (max_upd == 0 && max_k > 0 && root_dataflow()) return 2;  // assembly, root kernel
   const int W = lookahead_width(max_upd);
   if (max_k > W && level_fronts <= kLookaheadMaxFronts) {
     const int nsb = (max_k + W - 1) / W;

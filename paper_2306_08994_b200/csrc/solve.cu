@@ -146,6 +146,23 @@ __global__ void __launch_bounds__(G* GPC)
   }
   // update rows: w_r - l_r . w_piv (row-contiguous panel reads), straight out
   double* out = w_out + f * out_rows * ldr + col0;
+  if (!STAGE && k > 4) {
+    // one column, rows wider than a sector: a thread's whole row is requested
+    // in bursts of 8 entries (every sector of the row in flight together)
+    for (int r = k + t; r < m; r += G) {
+      const double* lr = Pg + (long long)r * kp;
+      double acc = W[r];
+      for (int c0 = 0; c0 < k; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = c0 + q < k ? __ldg(lr + c0 + q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc -= v[q] * W[min(c0 + q, k - 1)];
+      }
+      out[r - k] = acc;
+    }
+    return;
+  }
   for (int e = nK + t; e < nW; e += G) {
     const int r = e / nr, j = e - r * nr;
     double acc = W[e];
@@ -205,7 +222,26 @@ __global__ void __launch_bounds__(G* GPC)
     }
   }
   group_sync<G>(bar);
-  if (m > k) {
+  if (m > k && !STAGE && k > G) {
+    // one column: thread t owns columns t + qG, so a row's entries are all
+    // requested in the same iteration (each sector fetched once)
+    for (int cb = t; cb < k; cb += 4 * G) {
+      double acc[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[q] = cb + q * G < k ? X[cb + q * G] : 0.0;
+      for (int r = k; r < m; r++) {
+        const double xr = X[r];
+        const double* lr = Pg + (long long)r * kp;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (cb + q * G < k) acc[q] -= __ldg(lr + cb + q * G) * xr;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (cb + q * G < k) X[cb + q * G] = acc[q];
+    }
+    group_sync<G>(bar);
+  } else if (m > k) {
     for (int e = t; e < nK; e += G) {
       const int c = e / nr, j = e - c * nr;
       double acc = X[e];

@@ -13,7 +13,7 @@ static const char* kNames[K_COUNT] = {
     "large_diag_kernel", "large_block_kernel", "large_update_kernel<2> (trsm)",
     "large_update_kernel<0> (panel)", "large_update_kernel<1> (schur)",
     "large_diag_finalize_kernel", "solve_fwd_small", "solve_bwd_small", "solve_gather_bwd",
-    "solve_fwd_wave", "solve_bwd_wave", "permute_rows_kernel"};
+    "solve_fwd_wave", "solve_bwd_wave", "permute_rows_kernel", "large_root_kernel"};
 
 struct Pending {
   int cls;
