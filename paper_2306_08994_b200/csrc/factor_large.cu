@@ -988,22 +988,155 @@ static bool root_dataflow() {  // TFB_ROOT_DATAFLOW=0 selects the lookahead path
 
 // ------------------------------------------------------------- root fronts
 // Fronts without a Schur block (the root, m == k): one persistent launch that
-// factors the whole front as a dataflow over its 64x64 lower tiles (i, l),
-// left-looking.  Tiles are dealt in column-major order from an atomic
-// counter, so a tile only waits on tiles dealt before it to running CTAs (no
-// deadlock, whatever the residency).  Tile (i, l) accumulates
-// sum_{j<l} L_ij D_j L_lj^T as the columns j are published (flags,
-// acquire/release), subtracts it from its assembled value, then either
-// factors it (i == l: diag64_smem, l and d into the panel, aux block) or
-// solves it (i > l: L_il = A M_l^T D_l^-1) and publishes it.  The pivot chain
-// is one diagonal factorization + one tile solve + one 64-deep product per
-// column, with no launch gaps; sums run in a fixed order (deterministic).
+// factors the front as a dataflow over its 64x64 lower tiles (i, l).
+//   chain CTA (one per front): for every column l, takes the partial
+//     diagonal tile A_ll - sum_{j<l-1}, applies column l-1 itself (it still
+//     holds L_{l,l-1} and d_{l-1}), factors it (diag64_smem: l, d, inverse M_l)
+//     and publishes it; then solves the sub-diagonal tile
+//     L_{l+1,l} = A M_l^T D_l^-1 from its partial sum and publishes it.  The
+//     pivot chain therefore never leaves one CTA's shared memory.
+//   tile CTAs: the other tiles, dealt in column-major order from an atomic
+//     counter (a tile only waits on tiles dealt before it or on the chain, so
+//     the schedule cannot deadlock).  Tile (i, l) accumulates
+//     sum_j L_ij D_j L_lj^T left-looking as the columns j are published
+//     (flags, acquire/release); diagonal and sub-diagonal tiles hand their
+//     partial sums (columns j < l-1 resp. j < l) to the chain through the
+//     panel, the others solve themselves with the published M_l.
+// Sums run in a fixed order: results are deterministic.
 using GRoot = GemmCfg<64, 64, 16, 2>;
-constexpr size_t kRootSmem = sizeof(double) * (2 * NB * DLD + NB);
-static_assert(GRoot::smem <= kRootSmem, "GEMM staging fits the diagonal-block buffers");
+constexpr size_t kRootSmem = sizeof(double) * (3 * NB * DLD + 2 * NB);
+static_assert(GRoot::smem <= kRootSmem, "GEMM staging fits the tile buffers");
 
 __device__ __forceinline__ void root_wait(const int* flag) {
   while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+}
+__device__ __forceinline__ void root_publish(int* flag) {  // after a CTA barrier
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(flag, 1);
+  }
+}
+__device__ __forceinline__ long long root_clock() {
+  long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  return ns;
+}
+
+// acc (4x2 warps of 16x32, DMMA fragments) = sum_t A[r][t] * s_t * B[c][t], t < 64,
+// A and B in shared memory with row stride DLD (s == nullptr: s_t = 1)
+__device__ __forceinline__ void root_tile_product(double (&acc)[GRoot::MI][GRoot::NJ][2],
+                                                  double (*A)[DLD], double (*B)[DLD],
+                                                  const double* sc) {
+  constexpr int MI = GRoot::MI, NJ = GRoot::NJ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int a = 0; a < MI; a++)
+#pragma unroll
+    for (int b = 0; b < NJ; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < NB; ks += 4) {
+    const double s = sc ? sc[ks + tq] : 1.0;
+    double af[MI], bf[NJ];
+#pragma unroll
+    for (int a = 0; a < MI; a++) af[a] = A[wy * GRoot::WM + a * 8 + g8][ks + tq] * s;
+#pragma unroll
+    for (int b = 0; b < NJ; b++) bf[b] = B[wx * GRoot::WN + b * 8 + g8][ks + tq];
+#pragma unroll
+    for (int a = 0; a < MI; a++)
+#pragma unroll
+      for (int b = 0; b < NJ; b++) dmma884(acc[a][b], af[a], bf[b]);
+  }
+}
+
+// The pivot chain of front f (one CTA).
+__device__ void root_chain(const LevelArgs& L, double* factors, double threshold,
+                           unsigned long long* err, long long f, int T, int* done,
+                           const int* part_diag, const int* part_sub, long long* trace) {
+  extern __shared__ __align__(16) double rsm[];
+  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm);
+  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + NB * DLD);
+  double(*S)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + 2 * NB * DLD);
+  double* dv = rsm + 3 * NB * DLD;
+  double* dprev = dv + NB;
+  constexpr int MI = GRoot::MI, NJ = GRoot::NJ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
+  const Shape s = front_shape(L, f);
+  const int k = s.k, kp = s.kp;
+  double* Pf = factors + f * L.fac_stride;
+  double* dvec = Pf + (long long)s.m * kp;
+  for (int l = 0; l < T; l++) {
+    const int c0 = l * NB, kb = min(NB, k - c0);
+    if (kb <= 0) break;
+    if (tid == 0) root_wait(part_diag + l);
+    __syncthreads();
+    if (trace && tid == 0) trace[l * 8 + 0] = root_clock();
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int a = e >> 6, b = e & 63;
+      D[a][b] = (a < kb && b <= a) ? Pf[(long long)(c0 + a) * kp + c0 + b] : (a == b ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    if (l > 0) {  // column l-1: D -= L_{l,l-1} D_{l-1} L_{l,l-1}^T
+      double acc[MI][NJ][2];
+      root_tile_product(acc, S, S, dprev);
+#pragma unroll
+      for (int a = 0; a < MI; a++)
+#pragma unroll
+        for (int b = 0; b < NJ; b++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+            if (rl < kb && cl <= rl) D[rl][cl] -= acc[a][b][h];
+          }
+      __syncthreads();
+    }
+    diag64_smem<256>(D, Mi, dv, kb);
+    write_aux64<256>(L.aux + f * L.aux_stride + (long long)l * NB * NB, D, Mi, dv, kb);
+    for (int c = tid; c < kb; c += 256) {
+      dvec[c0 + c] = dv[c];
+      if (fabs(dv[c]) <= threshold)
+        record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + c0 + c));
+    }
+    __syncthreads();
+    root_publish(done + l * T + l);
+    if (trace && tid == 0) trace[l * 8 + 1] = root_clock();
+    // l and d into the panel (no other tile reads the diagonal tile's values)
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int a = e >> 6, b = e & 63;
+      if (a < kb && b <= a) Pf[(long long)(c0 + a) * kp + c0 + b] = D[a][b];
+    }
+    const int r0 = c0 + NB;
+    if (r0 >= k) break;
+    const int nA = min(NB, k - r0);
+    if (tid == 0) root_wait(part_sub + l + 1);
+    __syncthreads();
+    if (trace && tid == 0) trace[l * 8 + 2] = root_clock();
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int a = e >> 6, b = e & 63;
+      S[a][b] = (a < nA && b < kb) ? Pf[(long long)(r0 + a) * kp + c0 + b] : 0.0;
+    }
+    __syncthreads();
+    double x[MI][NJ][2];
+    root_tile_product(x, S, Mi, nullptr);
+    __syncthreads();  // every read of S precedes its overwrite
+#pragma unroll
+    for (int a = 0; a < MI; a++)
+#pragma unroll
+      for (int b = 0; b < NJ; b++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+          const bool in = rl < nA && cl < kb;
+          const double v = in ? x[a][b][h] / dv[cl] : 0.0;
+          S[rl][cl] = v;
+          if (in) Pf[(long long)(r0 + rl) * kp + c0 + cl] = v;
+        }
+    if (tid < NB) dprev[tid] = dv[tid];
+    __syncthreads();
+    root_publish(done + (l + 1) * T + l);
+    if (trace && tid == 0) trace[l * 8 + 3] = root_clock();
+  }
 }
 
 __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double* factors,
@@ -1013,25 +1146,34 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
   constexpr int BK = GRoot::BK, ST = GRoot::ST, LD = GRoot::LD, MI = GRoot::MI, NJ = GRoot::NJ;
   extern __shared__ __align__(16) double rsm[];
   __shared__ int s_tile;
-  double* As = rsm;                 // GEMM staging [ST][64][LD], [ST][64][LD], [ST][BK]
+  const int nf = L.n_fronts;
+  int* done = flags;                               // [nf][T][T] final tiles
+  int* part_diag = done + (long long)nf * T * T;   // [nf][T] partial diagonal tiles
+  int* part_sub = part_diag + (long long)nf * T;   // [nf][T] partial sub-diagonal tiles
+  int* counter = part_sub + (long long)nf * T;
+  if (blockIdx.x < (unsigned)nf) {
+    root_chain(L, factors, threshold, err, blockIdx.x, T, done + (long long)blockIdx.x * T * T,
+               part_diag + (long long)blockIdx.x * T, part_sub + (long long)blockIdx.x * T,
+               blockIdx.x == 0 ? trace : nullptr);
+    return;
+  }
+  double* As = rsm;  // GEMM staging [ST][64][LD], [ST][64][LD], [ST][BK]
   double* Bs = As + ST * NB * LD;
   double* Ds = Bs + ST * NB * LD;
-  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm);             // tile / diagonal block
-  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + NB * DLD);  // inverse block
+  double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm);             // tile
+  double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + NB * DLD);  // M_l
   double* dv = rsm + 2 * NB * DLD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
-  const long long per_front = (long long)T * (T + 1) / 2;
-  const long long ntiles = per_front * L.n_fronts;
-  int* counter = flags + (long long)L.n_fronts * T * T;
+  const long long ntiles = (long long)T * (T + 1) / 2 * nf;
   for (;;) {
     __syncthreads();  // shared memory is reused tile to tile
     if (tid == 0) s_tile = atomicAdd(counter, 1);
     __syncthreads();
     const long long t = s_tile;
     if (t >= ntiles) return;
-    const long long f = t % L.n_fronts;
-    long long rr = t / L.n_fronts;
+    const long long f = t % nf;
+    long long rr = t / nf;
     int l = 0;
     while (rr >= T - l) rr -= T - l++;
     const int i = l + (int)rr;
@@ -1041,9 +1183,11 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
     if (r0 >= k) continue;  // beyond this front (smaller than the level's largest)
     const int nA = min(NB, k - r0), nB = min(NB, k - c0);
     double* Pf = factors + f * L.fac_stride;
-    double* dvec = Pf + (long long)s.m * kp;
-    int* fl = flags + f * T * T;
-    const int nk = l * (NB / BK);
+    const double* dvec = Pf + (long long)s.m * kp;
+    int* fl = done + f * T * T;
+    // the chain applies the last column to the diagonal tile itself
+    const int ncols = i == l ? max(l - 1, 0) : l;
+    const int nk = ncols * (NB / BK);
 
     auto issue = [&](int it) {
       const int stage = it % ST, kt = it * BK;
@@ -1059,7 +1203,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
       }
       if (tid < CPR) cp_async16(Ds + stage * BK + tid * 2, dvec + kt + tid * 2, true);
     };
-    // column j of the product is ready once tiles (i, j) and (l, j) are published
+    // column j of the product is ready once tiles (i, j) and (l, j) are final
     auto wait_col = [&](int it) {
       if (tid == 0 && (it % (NB / BK)) == 0) {
         const int j = it / (NB / BK);
@@ -1105,90 +1249,59 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
     }
     cp_async_wait<0>();
     __syncthreads();  // staging buffers become D / Mi
-    auto stamp = [&](int slot) {
-      if (trace && tid == 0 && f == 0 && (i == l || i == l + 1)) {
-        long long ns;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ns));
-        trace[(long long)l * 8 + (i == l ? 0 : 4) + slot] = ns;
-      }
-    };
-    stamp(0);
 
-    // A = assembled tile - accumulated product, into D (unit rows/zeros outside)
+    if (i <= l + 1) {
+      // partial sum for the chain: A - sum, in place
+      if (nk > 0) {
 #pragma unroll
-    for (int a = 0; a < MI; a++) {
-      const int rl = wy * GRoot::WM + a * 8 + g8;
+        for (int a = 0; a < MI; a++)
+#pragma unroll
+          for (int b = 0; b < NJ; b++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+              if (rl < nA && cl < nB && (i != l || cl <= rl))
+                Pf[(long long)(r0 + rl) * kp + c0 + cl] -= acc[a][b][h];
+            }
+      }
+      __syncthreads();
+      root_publish(i == l ? part_diag + f * T + l : part_sub + f * T + i);
+      continue;
+    }
+    // A = assembled tile - product, into D
+#pragma unroll
+    for (int a = 0; a < MI; a++)
 #pragma unroll
       for (int b = 0; b < NJ; b++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          const int cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
-          const bool in = rl < nA && cl < nB && (i != l || cl <= rl);
-          D[rl][cl] = in ? Pf[(long long)(r0 + rl) * kp + c0 + cl] - acc[a][b][h]
-                         : (rl == cl ? 1.0 : 0.0);
+          const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+          D[rl][cl] = (rl < nA && cl < nB) ? Pf[(long long)(r0 + rl) * kp + c0 + cl] - acc[a][b][h]
+                                           : 0.0;
         }
-    }
-    if (i == l) {
-      __syncthreads();
-      diag64_smem<256>(D, Mi, dv, nB);
-      stamp(1);
-      for (int e = tid; e < NB * NB; e += 256) {
-        const int a = e >> 6, b = e & 63;
-        if (a < nB && b <= a) Pf[(long long)(r0 + a) * kp + c0 + b] = D[a][b];
-      }
-      for (int c = tid; c < nB; c += 256) {
-        dvec[c0 + c] = dv[c];
-        if (fabs(dv[c]) <= threshold)
-          record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + c0 + c));
-      }
-      write_aux64<256>(L.aux + f * L.aux_stride + (long long)l * NB * NB, D, Mi, dv, nB);
-    } else {
-      // L_il = A M_l^T D_l^-1 (M_l: strict lower part of the aux block)
-      if (tid == 0) root_wait(fl + l * T + l);
-      stamp(1);
-      __syncthreads();
-      const double* M = L.aux + f * L.aux_stride + (long long)l * NB * NB;
-      for (int e = tid; e < NB * NB; e += 256) {
-        const int a = e >> 6, b = e & 63;
-        Mi[a][b] = b < a ? M[e] : (b == a ? 1.0 : 0.0);
-      }
-      if (tid < NB) dv[tid] = tid < nB ? dvec[c0 + tid] : 1.0;
-      __syncthreads();
-      double x[MI][NJ][2];
-#pragma unroll
-      for (int a = 0; a < MI; a++)
-#pragma unroll
-        for (int b = 0; b < NJ; b++) x[a][b][0] = x[a][b][1] = 0.0;
-#pragma unroll 4
-      for (int ks = 0; ks < NB; ks += 4) {
-        double af[MI], bf[NJ];
-#pragma unroll
-        for (int a = 0; a < MI; a++) af[a] = D[wy * GRoot::WM + a * 8 + g8][ks + tq];
-#pragma unroll
-        for (int b = 0; b < NJ; b++) bf[b] = Mi[wx * GRoot::WN + b * 8 + g8][ks + tq];
-#pragma unroll
-        for (int a = 0; a < MI; a++)
-#pragma unroll
-          for (int b = 0; b < NJ; b++) dmma884(x[a][b], af[a], bf[b]);
-      }
-#pragma unroll
-      for (int a = 0; a < MI; a++) {
-        const int rl = wy * GRoot::WM + a * 8 + g8;
-#pragma unroll
-        for (int b = 0; b < NJ; b++)
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
-            if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] / dv[cl];
-          }
-      }
-    }
+    // L_il = A M_l^T D_l^-1 (M_l: strict lower part of the published aux block)
+    if (tid == 0) root_wait(fl + l * T + l);
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_gpu(fl + i * T + l, 1);
+    const double* M = L.aux + f * L.aux_stride + (long long)l * NB * NB;
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int a = e >> 6, b = e & 63;
+      Mi[a][b] = b < a ? M[e] : (b == a ? 1.0 : 0.0);
     }
-    stamp(2);
+    if (tid < NB) dv[tid] = tid < nB ? dvec[c0 + tid] : 1.0;
+    __syncthreads();
+    double x[MI][NJ][2];
+    root_tile_product(x, D, Mi, nullptr);
+#pragma unroll
+    for (int a = 0; a < MI; a++)
+#pragma unroll
+      for (int b = 0; b < NJ; b++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
+          if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] / dv[cl];
+        }
+    __syncthreads();
+    root_publish(fl + i * T + l);
   }
 }
 
@@ -1211,7 +1324,8 @@ static int* root_flags(long long ints) {  // per-device scratch, grown on demand
 static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
                                unsigned long long* err, cudaStream_t st) {
   const int T = (L.max_k + NB - 1) / NB;
-  const long long nflags = (long long)L.n_fronts * T * T + 1;
+  const long long nf = L.n_fronts;
+  const long long nflags = nf * T * T + 2 * nf * T + 1;
   int* flags = root_flags(nflags);
   if (!flags) return cudaErrorMemoryAllocation;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * nflags, st);
@@ -1226,15 +1340,19 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long ntiles = (long long)L.n_fronts * T * (T + 1) / 2;
-  const unsigned grid = (unsigned)std::max(1LL, std::min(ntiles, (long long)sms * occ));
-  timer_begin(K_ROOT, st);
+  // chain CTAs + tile CTAs, all co-resident (tile CTAs wait on the chain)
+  const long long ntiles = nf * T * (T + 1) / 2;
+  const long long cap = (long long)sms * occ;
+  if (nf + 1 > cap) return cudaErrorInvalidConfiguration;
+  const unsigned grid = (unsigned)std::min(ntiles + nf, cap);
   static long long* trace = nullptr;
   if (getenv("TFB_ROOT_TRACE") && !trace) {
     cudaMalloc(&trace, sizeof(long long) * 8 * 4096);
     cudaMemset(trace, 0, sizeof(long long) * 8 * 4096);
   }
+  timer_begin(K_ROOT, st);
   large_root_kernel<<<grid, 256, kRootSmem, st>>>(L, factors, thr, err, flags, T, trace);
+  timer_end(st);
   if (trace && T <= 4096) {
     static std::vector<long long> h;
     h.resize(8 * T);
@@ -1242,11 +1360,10 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
     cudaStreamSynchronize(st);
     const long long t0 = h[0];
     for (int l = 0; l < T; l++)
-      fprintf(stderr, "col %3d diag: ready %8.1f done %8.1f pub %8.1f | trsm: ready %8.1f pub %8.1f us\n", l,
+      fprintf(stderr, "col %3d diag ready %8.1f pub %8.1f | sub ready %8.1f pub %8.1f us\n", l,
               (h[8 * l] - t0) * 1e-3, (h[8 * l + 1] - t0) * 1e-3, (h[8 * l + 2] - t0) * 1e-3,
-              (h[8 * l + 5] - t0) * 1e-3, (h[8 * l + 6] - t0) * 1e-3);
+              (h[8 * l + 3] - t0) * 1e-3);
   }
-  timer_end(st);
   return cudaGetLastError();
 }
 
