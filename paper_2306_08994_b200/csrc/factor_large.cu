@@ -1049,49 +1049,144 @@ __device__ __forceinline__ void root_tile_product(double (&acc)[GRoot::MI][GRoot
   }
 }
 
+// D[r][c] -= sum_t S[r][t] s_t S[c][t] for c <= r < kb: the 36 lower 8x8
+// tiles dealt to the 8 warps (balanced), DMMA over t < 64.
+__device__ __forceinline__ void root_syrk_lower(double (*D)[DLD], double (*S)[DLD],
+                                                const double* sc, int kb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, tq = lane & 3;
+  constexpr int Q = 5;  // ceil(36 / 8)
+  double acc[Q][2];
+  int I[Q], J[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int tile = min(warp + 8 * q, 35);
+    I[q] = tri_row32(tile);
+    J[q] = tile - tri32(I[q], 0);
+    acc[q][0] = acc[q][1] = 0.0;
+  }
+#pragma unroll 4
+  for (int ks = 0; ks < NB; ks += 4) {
+    const double s = sc[ks + tq];
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+      if (warp + 8 * q < 36)
+        dmma884(acc[q], S[8 * I[q] + g8][ks + tq] * s, S[8 * J[q] + g8][ks + tq]);
+  }
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    if (warp + 8 * q >= 36) continue;
+    const int r = 8 * I[q] + g8;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int c = 8 * J[q] + 2 * tq + h;
+      if (r < kb && c <= r) D[r][c] -= acc[q][h];
+    }
+  }
+}
+
+// x = S M^T for unit-lower M (only t <= n contributes to column n): warp w
+// owns rows 8w..8w+7 and all eight column blocks (balanced, 72 DMMAs each).
+// Fragment x[cb][h] is entry (8w + lane/4, 8cb + 2(lane%4) + h).
+__device__ __forceinline__ void root_trsm_rows(double (&x)[8][2], double (*S)[DLD],
+                                               double (*M)[DLD]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int cb = 0; cb < 8; cb++) x[cb][0] = x[cb][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < NB; ks += 4) {
+    const double a = S[8 * warp + g8][ks + tq];
+#pragma unroll
+    for (int cb = 0; cb < 8; cb++)
+      if (ks < 8 * cb + 8) dmma884(x[cb], a, M[8 * cb + g8][ks + tq]);
+  }
+}
+
 // The pivot chain of front f (one CTA).
 __device__ void root_chain(const LevelArgs& L, double* factors, double threshold,
                            unsigned long long* err, long long f, int T, int* done,
                            const int* part_diag, const int* part_sub, long long* trace) {
   extern __shared__ __align__(16) double rsm[];
+  __shared__ int s_ready;
   double(*D)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm);
   double(*Mi)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + NB * DLD);
   double(*S)[DLD] = reinterpret_cast<double(*)[DLD]>(rsm + 2 * NB * DLD);
   double* dv = rsm + 3 * NB * DLD;
   double* dprev = dv + NB;
-  constexpr int MI = GRoot::MI, NJ = GRoot::NJ;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g8 = lane >> 2, tq = lane & 3;
   const Shape s = front_shape(L, f);
   const int k = s.k, kp = s.kp;
   double* Pf = factors + f * L.fac_stride;
   double* dvec = Pf + (long long)s.m * kp;
+  // rows [row0, row0 + nr) x columns [col0, col0 + nc) of the panel into X
+  // (asynchronous, zeros outside)
+  auto load_tile = [&](double(*X)[DLD], int row0, int nr, int col0, int nc) {
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int a = e >> 6, b = e & 63;
+      const bool v = a < nr && b < nc;
+      cp_async8(&X[a][b], v ? Pf + (long long)(row0 + a) * kp + col0 + b : Pf, v);
+    }
+    cp_async_commit();
+  };
+  // non-blocking probe of a flag, broadcast to the CTA (the caller syncs)
+  auto probe = [&](const int* flag, bool want) {
+    if (tid == 0) s_ready = want ? ld_acquire_gpu(flag) : 0;
+  };
+  bool d_pref = false;
   for (int l = 0; l < T; l++) {
     const int c0 = l * NB, kb = min(NB, k - c0);
     if (kb <= 0) break;
-    if (tid == 0) root_wait(part_diag + l);
+    const int r0 = c0 + NB, nA = min(NB, k - r0);
+    if (!d_pref) {
+      if (tid == 0) root_wait(part_diag + l);
+      __syncthreads();
+      load_tile(D, c0, kb, c0, kb);
+    }
+    cp_async_wait<0>();
     __syncthreads();
     if (trace && tid == 0) trace[l * 8 + 0] = root_clock();
-    for (int e = tid; e < NB * NB; e += 256) {
+    for (int e = tid; e < NB * NB; e += 256) {  // unit rows / zeros outside the lower part
       const int a = e >> 6, b = e & 63;
-      D[a][b] = (a < kb && b <= a) ? Pf[(long long)(c0 + a) * kp + c0 + b] : (a == b ? 1.0 : 0.0);
+      if (!(a < kb && b <= a)) D[a][b] = a == b ? 1.0 : 0.0;
     }
     __syncthreads();
-    if (l > 0) {  // column l-1: D -= L_{l,l-1} D_{l-1} L_{l,l-1}^T
-      double acc[MI][NJ][2];
-      root_tile_product(acc, S, S, dprev);
-#pragma unroll
-      for (int a = 0; a < MI; a++)
-#pragma unroll
-        for (int b = 0; b < NJ; b++)
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
-            if (rl < kb && cl <= rl) D[rl][cl] -= acc[a][b][h];
-          }
-      __syncthreads();
-    }
+    if (l > 0) root_syrk_lower(D, S, dprev, kb);  // column l-1: D -= L_{l,l-1} D_{l-1} L^T
+    probe(part_sub + l + 1, nA > 0);
+    __syncthreads();
+    const bool s_pref = s_ready != 0;
+    if (s_pref) load_tile(S, r0, nA, c0, kb);  // overlaps the diagonal factorization
     diag64_smem<256>(D, Mi, dv, kb);
+    if (trace && tid == 0) trace[l * 8 + 1] = root_clock();
+    if (nA > 0) {
+      // sub-diagonal tile: L_{l+1,l} = A M_l^T D_l^-1, kept in S for column l+1
+      if (!s_pref) {
+        if (tid == 0) root_wait(part_sub + l + 1);
+        __syncthreads();
+        load_tile(S, r0, nA, c0, kb);
+      }
+      if (tid < NB) dprev[tid] = rcp_nr(dv[tid]);
+      cp_async_wait<0>();
+      __syncthreads();
+      double x[8][2];
+      root_trsm_rows(x, S, Mi);
+      __syncthreads();  // every read of S precedes its overwrite
+      const int rl = 8 * warp + g8;
+#pragma unroll
+      for (int cb = 0; cb < 8; cb++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int cl = 8 * cb + 2 * tq + h;
+          const bool in = rl < nA && cl < kb;
+          const double v = in ? x[cb][h] * dprev[cl] : 0.0;  // dprev holds 1/d here
+          S[rl][cl] = v;
+          if (in) Pf[(long long)(r0 + rl) * kp + c0 + cl] = v;
+        }
+      __syncthreads();  // every 1/d read
+      if (tid < NB) dprev[tid] = dv[tid];
+      __syncthreads();
+      root_publish(done + (l + 1) * T + l);
+      if (trace && tid == 0) trace[l * 8 + 2] = root_clock();
+    }
+    // d and the aux block (M_l for the other tiles' solves), then the panel
     write_aux64<256>(L.aux + f * L.aux_stride + (long long)l * NB * NB, D, Mi, dv, kb);
     for (int c = tid; c < kb; c += 256) {
       dvec[c0 + c] = dv[c];
@@ -1100,42 +1195,16 @@ __device__ void root_chain(const LevelArgs& L, double* factors, double threshold
     }
     __syncthreads();
     root_publish(done + l * T + l);
-    if (trace && tid == 0) trace[l * 8 + 1] = root_clock();
-    // l and d into the panel (no other tile reads the diagonal tile's values)
     for (int e = tid; e < NB * NB; e += 256) {
       const int a = e >> 6, b = e & 63;
       if (a < kb && b <= a) Pf[(long long)(c0 + a) * kp + c0 + b] = D[a][b];
     }
-    const int r0 = c0 + NB;
-    if (r0 >= k) break;
-    const int nA = min(NB, k - r0);
-    if (tid == 0) root_wait(part_sub + l + 1);
-    __syncthreads();
-    if (trace && tid == 0) trace[l * 8 + 2] = root_clock();
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int a = e >> 6, b = e & 63;
-      S[a][b] = (a < nA && b < kb) ? Pf[(long long)(r0 + a) * kp + c0 + b] : 0.0;
-    }
-    __syncthreads();
-    double x[MI][NJ][2];
-    root_tile_product(x, S, Mi, nullptr);
-    __syncthreads();  // every read of S precedes its overwrite
-#pragma unroll
-    for (int a = 0; a < MI; a++)
-#pragma unroll
-      for (int b = 0; b < NJ; b++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
-          const bool in = rl < nA && cl < kb;
-          const double v = in ? x[a][b][h] / dv[cl] : 0.0;
-          S[rl][cl] = v;
-          if (in) Pf[(long long)(r0 + rl) * kp + c0 + cl] = v;
-        }
-    if (tid < NB) dprev[tid] = dv[tid];
-    __syncthreads();
-    root_publish(done + (l + 1) * T + l);
     if (trace && tid == 0) trace[l * 8 + 3] = root_clock();
+    // prefetch the next partial diagonal tile when it is ready
+    probe(part_diag + l + 1, nA > 0);
+    __syncthreads();  // also: D fully read
+    d_pref = s_ready != 0;
+    if (d_pref) load_tile(D, r0, nA, r0, nA);
   }
 }
 
@@ -1151,7 +1220,13 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
   int* part_diag = done + (long long)nf * T * T;   // [nf][T] partial diagonal tiles
   int* part_sub = part_diag + (long long)nf * T;   // [nf][T] partial sub-diagonal tiles
   int* counter = part_sub + (long long)nf * T;
+  int* chain_sm = counter + 1;  // [nf] SM of each chain CTA, + 1 (0: not yet known)
   if (blockIdx.x < (unsigned)nf) {
+    if (threadIdx.x == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      st_release_gpu(chain_sm + blockIdx.x, (int)sm + 1);
+    }
     root_chain(L, factors, threshold, err, blockIdx.x, T, done + (long long)blockIdx.x * T * T,
                part_diag + (long long)blockIdx.x * T, part_sub + (long long)blockIdx.x * T,
                blockIdx.x == 0 ? trace : nullptr);
@@ -1166,6 +1241,20 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
   const long long ntiles = (long long)T * (T + 1) / 2 * nf;
+  // tile CTAs leave the chain CTAs' SMs to them (the chain is the critical path)
+  if (tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    int mine = 0;
+    for (int c = 0; c < nf; c++) {
+      int v;
+      while ((v = ld_acquire_gpu(chain_sm + c)) == 0) __nanosleep(32);
+      mine |= v == (int)sm + 1;
+    }
+    s_tile = mine;
+  }
+  __syncthreads();
+  if (s_tile) return;
   for (;;) {
     __syncthreads();  // shared memory is reused tile to tile
     if (tid == 0) s_tile = atomicAdd(counter, 1);
@@ -1287,7 +1376,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
       const int a = e >> 6, b = e & 63;
       Mi[a][b] = b < a ? M[e] : (b == a ? 1.0 : 0.0);
     }
-    if (tid < NB) dv[tid] = tid < nB ? dvec[c0 + tid] : 1.0;
+    if (tid < NB) dv[tid] = tid < nB ? rcp_nr(dvec[c0 + tid]) : 1.0;
     __syncthreads();
     double x[MI][NJ][2];
     root_tile_product(x, D, Mi, nullptr);
@@ -1298,7 +1387,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int rl = wy * GRoot::WM + a * 8 + g8, cl = wx * GRoot::WN + b * 8 + 2 * tq + h;
-          if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] / dv[cl];
+          if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] * dv[cl];
         }
     __syncthreads();
     root_publish(fl + i * T + l);
@@ -1325,7 +1414,7 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
                                unsigned long long* err, cudaStream_t st) {
   const int T = (L.max_k + NB - 1) / NB;
   const long long nf = L.n_fronts;
-  const long long nflags = nf * T * T + 2 * nf * T + 1;
+  const long long nflags = nf * T * T + 2 * nf * T + 1 + nf;
   int* flags = root_flags(nflags);
   if (!flags) return cudaErrorMemoryAllocation;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * nflags, st);
@@ -1343,8 +1432,9 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
   // chain CTAs + tile CTAs, all co-resident (tile CTAs wait on the chain)
   const long long ntiles = nf * T * (T + 1) / 2;
   const long long cap = (long long)sms * occ;
-  if (nf + 1 > cap) return cudaErrorInvalidConfiguration;
-  const unsigned grid = (unsigned)std::min(ntiles + nf, cap);
+  // tile CTAs that land next to a chain CTA exit: keep at least one other
+  if (nf * occ + 1 > cap) return cudaErrorInvalidConfiguration;
+  const unsigned grid = (unsigned)std::min(std::max(ntiles + nf, nf * occ + 1), cap);
   static long long* trace = nullptr;
   if (getenv("TFB_ROOT_TRACE") && !trace) {
     cudaMalloc(&trace, sizeof(long long) * 8 * 4096);
@@ -1360,7 +1450,7 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
     cudaStreamSynchronize(st);
     const long long t0 = h[0];
     for (int l = 0; l < T; l++)
-      fprintf(stderr, "col %3d diag ready %8.1f pub %8.1f | sub ready %8.1f pub %8.1f us\n", l,
+      fprintf(stderr, "col %3d ready %8.1f diag %8.1f sub pub %8.1f diag pub %8.1f us\n", l,
               (h[8 * l] - t0) * 1e-3, (h[8 * l + 1] - t0) * 1e-3, (h[8 * l + 2] - t0) * 1e-3,
               (h[8 * l + 3] - t0) * 1e-3);
   }

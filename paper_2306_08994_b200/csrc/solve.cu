@@ -312,12 +312,6 @@ __device__ __forceinline__ void wave_publish(int* flag) {
     st_release(flag, 1);
   }
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
-               "r"(valid ? 8 : 0)
-               : "memory");
-}
 // T[i][c] = src[i * ld + c] for i < rows, c < cols (async 16-byte copies; src
 // and T rows 16-byte aligned).  Entries outside are left as they are: the tile
 // products below bound their sums and callers ignore out-of-range outputs.
