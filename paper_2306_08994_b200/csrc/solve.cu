@@ -692,6 +692,223 @@ __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
   }
 }
 
+// ------------------------------------------------- narrow large fronts
+// Large levels whose fronts have k <= 64 pivots (one diagonal block), one
+// right-hand side: a warp per front, the front's vector block in shared
+// memory.  Every panel row (and every row of the inverse block M) is read by
+// the warp as one coalesced request, lanes owning columns t = lane + 32q:
+//   forward : Y = M W_piv and W_r - L_r Y (row r >= k) are row dot products,
+//             reduced 32 rows at a time by a shuffle transpose-reduction;
+//   backward: z = y_piv - L21^T X_rows and x = M^T z accumulate per column,
+//             no reduction at all.
+// Summation orders are fixed (deterministic).
+constexpr int kNarrowWarps = 8;
+
+// v[j] (per lane) -> lane i returns sum over lanes of v[i]; 31 shuffles.
+__device__ __forceinline__ double transpose_reduce32(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; j++) {
+      const double send = up ? v[j] : v[j + off];
+      const double keep = up ? v[j + off] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <int Q>
+__global__ void __launch_bounds__(32 * kNarrowWarps)
+    solve_fwd_narrow(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
+                     const double* __restrict__ w_child, long long child_rows, double* w_out,
+                     long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double nsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kNarrowWarps + warp;
+  if (f >= L.n_fronts) return;  // warp-level work only (no CTA barriers)
+  double* W = nsm + (long long)warp * L.max_m;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  // 1. W = pivot-order RHS rows + the children's update rows
+  {
+    long long chs[2] = {0, 0};
+    int kc[2] = {0, 0};
+    for (int c = 0; c < s.nsrc; c++) {
+      chs[c] = 2 * (L.front_base + f) + c - C.front_base;
+      kc[c] = child_at0 ? 0 : C.pat[(size_t)C.pattern_of[chs[c]] * TF_PAT_WIDTH + TF_PAT_K];
+    }
+    const int* inv = L.maps + s.ioff;
+    for (int r = lane; r < m; r += 32) {
+      double v = r < k ? y[(piv + r) * ldr + col0] : 0.0;
+      for (int c = 0; c < s.nsrc; c++) {
+        const int i = __ldg(inv + c * m + r);
+        if (i >= 0) v += w_child[(chs[c] * child_rows + kc[c] + i) * ldr + col0];
+      }
+      W[r] = v;
+    }
+  }
+  __syncwarp();
+  // 2. Y = M W on the pivot rows (M: strict lower part of the aux block, unit diagonal)
+  const double* M = L.aux + f * L.aux_stride;
+  double wq[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) wq[q] = lane + 32 * q < k ? W[lane + 32 * q] : 0.0;
+  for (int n0 = 0; n0 < k; n0 += 32) {
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const int n = n0 + j;
+      double p = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int t = lane + 32 * q;
+        if (n < k && t < n) p += __ldg(M + n * TB + t) * wq[q];
+      }
+      v[j] = p;
+    }
+    const double red = transpose_reduce32(v);
+    const int n = n0 + lane;
+    if (n < k) {
+      const double yv = W[n] + red;
+      W[n] = yv;
+      y[(piv + n) * ldr + col0] = yv / Pf[(long long)m * kp + n];
+    }
+  }
+  __syncwarp();
+  // 3. update rows: W_r - L_r Y, 32 rows per round, straight out (in place: rows [k, m))
+  double yq[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) yq[q] = lane + 32 * q < k ? W[lane + 32 * q] : 0.0;
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int r0 = k; r0 < m; r0 += 32) {
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const int r = r0 + j;
+      double p = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int t = lane + 32 * q;
+        if (r < m && t < k) p += __ldg(Pf + (long long)r * kp + t) * yq[q];
+      }
+      v[j] = p;
+    }
+    const double red = transpose_reduce32(v);
+    const int r = r0 + lane;
+    if (r < m) out[(long long)r * ldr] = W[r] - red;
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(32 * kNarrowWarps)
+    solve_bwd_narrow(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
+                     const double* __restrict__ x_parent, long long parent_rows, double* x_out,
+                     long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double nsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kNarrowWarps + warp;
+  if (f >= L.n_fronts) return;
+  double* X = nsm + (long long)warp * L.max_m;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  // 1. X = pivot rows of y, shared rows gathered from the parent's block
+  const int* mp = nullptr;
+  const double* Xp = nullptr;
+  if (has_parent && m > k) {
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
+    mp = PA.maps + (((L.front_base + f) & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    Xp = x_parent + pf * parent_rows * ldr + col0;
+  }
+  for (int r = lane; r < m; r += 32)
+    X[r] = r < k ? y[(piv + r) * ldr + col0] : (mp ? Xp[(long long)__ldg(mp + r - k) * ldr] : 0.0);
+  __syncwarp();
+  // 2. z_c = y_c - sum_{r >= k} l_rc x_r (column c = lane + 32q)
+  double z[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) z[q] = 0.0;
+  int r = k;
+  for (; r + 3 < m; r += 4) {  // four rows in flight
+    double lv[4][Q];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int t = lane + 32 * q;
+        lv[u][q] = t < k ? __ldg(Pf + (long long)(r + u) * kp + t) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const double xr = X[r + u];
+#pragma unroll
+      for (int q = 0; q < Q; q++) z[q] += lv[u][q] * xr;
+    }
+  }
+  for (; r < m; r++) {
+    const double xr = X[r];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int t = lane + 32 * q;
+      if (t < k) z[q] += __ldg(Pf + (long long)r * kp + t) * xr;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int t = lane + 32 * q;
+    z[q] = t < k ? X[t] - z[q] : 0.0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < Q; q++)
+    if (lane + 32 * q < k) X[lane + 32 * q] = z[q];
+  __syncwarp();
+  // 3. x = M^T z: x_c = z_c + sum_{n > c} M(n, c) z_n (rows of M coalesced)
+  const double* M = L.aux + f * L.aux_stride;
+  double x[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) x[q] = z[q];
+  for (int n = 1; n < k; n++) {
+    const double zn = X[n];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int t = lane + 32 * q;
+      if (t < n) x[q] += __ldg(M + n * TB + t) * zn;
+    }
+  }
+  double* Xo = x_out + f * out_rows * ldr + col0;
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int t = lane + 32 * q;
+    if (t < k) {
+      y[(piv + t) * ldr + col0] = x[q];
+      Xo[(long long)t * ldr] = x[q];
+    }
+  }
+  for (int rr = k + lane; rr < m; rr += 32) Xo[(long long)rr * ldr] = X[rr];
+}
+
+static bool narrow_solve(const LevelArgs& L, int nrhs) {
+  static int v = -1;  // TFB_NARROW_SOLVE=0: wavefront kernels instead (A/B)
+  if (v < 0) {
+    const char* e = getenv("TFB_NARROW_SOLVE");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v && nrhs == 1 && L.max_k > 0 && L.max_k <= 2 * 32 &&
+         (size_t)kNarrowWarps * L.max_m * 8 <= 200 * 1024;
+}
+
+template <class K>
+static void narrow_attr(K kern, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 // ------------------------------------------------------------------ launch
 constexpr size_t kSmallSolveSmem = 160 * 1024;
 
@@ -833,6 +1050,22 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
   if (!level_is_large(L.is_leaf, L.max_m))
     return dispatch_small<true>(L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, y,
                                 nrhs, st);
+  if (narrow_solve(L, nrhs)) {
+    const size_t smem = (size_t)kNarrowWarps * L.max_m * 8;
+    const unsigned g = (unsigned)((L.n_fronts + kNarrowWarps - 1) / kNarrowWarps);
+    timer_begin(K_SOLVE_FWD_WAVE, st);
+    if (L.max_k <= 32) {
+      narrow_attr(solve_fwd_narrow<1>, smem);
+      solve_fwd_narrow<1><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
+                                                              child_rows, w_out, out_rows, y, nrhs, 0);
+    } else {
+      narrow_attr(solve_fwd_narrow<2>, smem);
+      solve_fwd_narrow<2><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
+                                                              child_rows, w_out, out_rows, y, nrhs, 0);
+    }
+    timer_end(st);
+    return cudaGetLastError();
+  }
   if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const int nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
   const int cw = std::min(nrhs, kWaveCols);
@@ -867,6 +1100,22 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   if (!level_is_large(L.is_leaf, L.max_m))
     return dispatch_small<false>(L, PA, has_parent, factors, x_parent, parent_rows, x_out,
                                  out_rows, y, nrhs, st);
+  if (narrow_solve(L, nrhs)) {
+    const size_t smem = (size_t)kNarrowWarps * L.max_m * 8;
+    const unsigned g = (unsigned)((L.n_fronts + kNarrowWarps - 1) / kNarrowWarps);
+    timer_begin(K_SOLVE_BWD_WAVE, st);
+    if (L.max_k <= 32) {
+      narrow_attr(solve_bwd_narrow<1>, smem);
+      solve_bwd_narrow<1><<<g, 32 * kNarrowWarps, smem, st>>>(L, PA, has_parent, factors, x_parent,
+                                                              parent_rows, x_out, out_rows, y, nrhs, 0);
+    } else {
+      narrow_attr(solve_bwd_narrow<2>, smem);
+      solve_bwd_narrow<2><<<g, 32 * kNarrowWarps, smem, st>>>(L, PA, has_parent, factors, x_parent,
+                                                              parent_rows, x_out, out_rows, y, nrhs, 0);
+    }
+    timer_end(st);
+    return cudaGetLastError();
+  }
   if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
@@ -903,6 +1152,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   if (!level_is_large(L.is_leaf, L.max_m)) return (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
+  if (narrow_solve(L, nrhs)) return 1;
   const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
   if (fwd) return slices;
   return 1 + (L.max_k > 0 ? slices : 0);
