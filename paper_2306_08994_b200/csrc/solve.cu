@@ -704,11 +704,36 @@ __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
 // Summation orders are fixed (deterministic).
 constexpr int kNarrowWarps = 8;
 
-// v[j] (per lane) -> lane i returns sum over lanes of v[i]; 31 shuffles.
-__device__ __forceinline__ double transpose_reduce32(double (&v)[32]) {
-  const int lane = threadIdx.x & 31;
+// 32 row dot products of one warp: sum_t A[r][t] v_t for rows r0 + g + 4j
+// (group g = lane / 8, j < 8), t < min(k, TRI ? r : k).  Lane (g, c) reads
+// columns [c*CW, c*CW + CW) of its group's rows with 16-byte loads, so each
+// warp request covers four whole rows; the eight partial sums of a group are
+// combined by a transpose-reduction over its lanes (7 shuffles per 8 rows).
+// Returns the sum for row r0 + g + 4c (lane (g, c)).
+template <int CW, bool TRI>
+__device__ __forceinline__ double rows32_dot(const double* __restrict__ A, int lda, int r0,
+                                             int rend, int k, const double (&vt)[CW]) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7, t0 = c * CW;
+  double v[8];
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
+  for (int j = 0; j < 8; j++) {
+    const int r = r0 + g + 4 * j;
+    const int lim = TRI ? min(k, r) : k;
+    double p = 0.0;
+    if (r < rend) {
+#pragma unroll
+      for (int h = 0; h < CW; h += 2) {
+        if (t0 + h < lim) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(A + (long long)r * lda + t0 + h));
+          p += x.x * vt[h];
+          if (t0 + h + 1 < lim) p += x.y * vt[h + 1];
+        }
+      }
+    }
+    v[j] = p;
+  }
+#pragma unroll
+  for (int off = 4; off >= 1; off >>= 1) {
     const bool up = (lane & off) != 0;
 #pragma unroll
     for (int j = 0; j < off; j++) {
@@ -720,7 +745,8 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32]) {
   return v[0];
 }
 
-template <int Q>
+// CW = panel columns per lane (8 lanes per row): 4 for k <= 32, 8 for k <= 64
+template <int CW>
 __global__ void __launch_bounds__(32 * kNarrowWarps)
     solve_fwd_narrow(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
                      const double* __restrict__ w_child, long long child_rows, double* w_out,
@@ -753,53 +779,40 @@ __global__ void __launch_bounds__(32 * kNarrowWarps)
     }
   }
   __syncwarp();
+  const int t0 = (lane & 7) * CW;
+  const int gr = (lane >> 3) + 4 * (lane & 7);  // row of the lane's reduced sum, within 32
   // 2. Y = M W on the pivot rows (M: strict lower part of the aux block, unit diagonal)
+  double vt[CW];
+#pragma unroll
+  for (int h = 0; h < CW; h++) vt[h] = t0 + h < k ? W[t0 + h] : 0.0;
   const double* M = L.aux + f * L.aux_stride;
-  double wq[Q];
+  double yv[2];
 #pragma unroll
-  for (int q = 0; q < Q; q++) wq[q] = lane + 32 * q < k ? W[lane + 32 * q] : 0.0;
-  for (int n0 = 0; n0 < k; n0 += 32) {
-    double v[32];
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      const int n = n0 + j;
-      double p = 0.0;
-#pragma unroll
-      for (int q = 0; q < Q; q++) {
-        const int t = lane + 32 * q;
-        if (n < k && t < n) p += __ldg(M + n * TB + t) * wq[q];
-      }
-      v[j] = p;
+  for (int b = 0; b < 2; b++) {
+    yv[b] = 0.0;
+    if (32 * b < k) {
+      const double red = rows32_dot<CW, true>(M, TB, 32 * b, k, k, vt);
+      const int n = 32 * b + gr;
+      if (n < k) yv[b] = W[n] + red;
     }
-    const double red = transpose_reduce32(v);
-    const int n = n0 + lane;
+  }
+  __syncwarp();  // every W read above precedes the stores below
+#pragma unroll
+  for (int b = 0; b < 2; b++) {
+    const int n = 32 * b + gr;
     if (n < k) {
-      const double yv = W[n] + red;
-      W[n] = yv;
-      y[(piv + n) * ldr + col0] = yv / Pf[(long long)m * kp + n];
+      W[n] = yv[b];
+      y[(piv + n) * ldr + col0] = yv[b] / Pf[(long long)m * kp + n];
     }
   }
   __syncwarp();
   // 3. update rows: W_r - L_r Y, 32 rows per round, straight out (in place: rows [k, m))
-  double yq[Q];
 #pragma unroll
-  for (int q = 0; q < Q; q++) yq[q] = lane + 32 * q < k ? W[lane + 32 * q] : 0.0;
+  for (int h = 0; h < CW; h++) vt[h] = t0 + h < k ? W[t0 + h] : 0.0;
   double* out = w_out + f * out_rows * ldr + col0;
   for (int r0 = k; r0 < m; r0 += 32) {
-    double v[32];
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      const int r = r0 + j;
-      double p = 0.0;
-#pragma unroll
-      for (int q = 0; q < Q; q++) {
-        const int t = lane + 32 * q;
-        if (r < m && t < k) p += __ldg(Pf + (long long)r * kp + t) * yq[q];
-      }
-      v[j] = p;
-    }
-    const double red = transpose_reduce32(v);
-    const int r = r0 + lane;
+    const double red = rows32_dot<CW, false>(Pf, kp, r0, m, k, vt);
+    const int r = r0 + gr;
     if (r < m) out[(long long)r * ldr] = W[r] - red;
   }
 }
@@ -1055,12 +1068,12 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
     const unsigned g = (unsigned)((L.n_fronts + kNarrowWarps - 1) / kNarrowWarps);
     timer_begin(K_SOLVE_FWD_WAVE, st);
     if (L.max_k <= 32) {
-      narrow_attr(solve_fwd_narrow<1>, smem);
-      solve_fwd_narrow<1><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
+      narrow_attr(solve_fwd_narrow<4>, smem);
+      solve_fwd_narrow<4><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
                                                               child_rows, w_out, out_rows, y, nrhs, 0);
     } else {
-      narrow_attr(solve_fwd_narrow<2>, smem);
-      solve_fwd_narrow<2><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
+      narrow_attr(solve_fwd_narrow<8>, smem);
+      solve_fwd_narrow<8><<<g, 32 * kNarrowWarps, smem, st>>>(L, C, child_at0, factors, w_child,
                                                               child_rows, w_out, out_rows, y, nrhs, 0);
     }
     timer_end(st);
