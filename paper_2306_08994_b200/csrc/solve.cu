@@ -907,6 +907,194 @@ __global__ void __launch_bounds__(32 * kNarrowWarps)
   for (int rr = k + lane; rr < m; rr += 32) Xo[(long long)rr * ldr] = X[rr];
 }
 
+// ------------------------------------------------- CTA-per-front sweeps
+// Levels with many fronts of k > 64 pivots, one right-hand side: a CTA per
+// front, the front's vector block in shared memory, blocked by the 64-wide
+// diagonal blocks of the factorization (inverses M_b from aux).  Every panel
+// entry is read once, by coalesced warp requests; no flags, no workspace.
+//   forward : per block b: Y_b = M_b W_b (two warps, rows32_dot), then
+//             W_r -= L[r, b] Y_b for every row below (32-row chunks dealt to
+//             the warps, eight lanes per row);
+//   backward: per block b (last first): z_b = X_b - L[rows below, b]^T X_rows
+//             (warps split the rows, lanes own columns, fixed-order combine),
+//             X_b = M_b^T z_b.
+__global__ void __launch_bounds__(256)
+    solve_fwd_front(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
+                    const double* __restrict__ w_child, long long child_rows, double* w_out,
+                    long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double fsm[];
+  double* W = fsm;
+  const long long f = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  {
+    long long chs[2] = {0, 0};
+    int kc[2] = {0, 0};
+    for (int c = 0; c < s.nsrc; c++) {
+      chs[c] = 2 * (L.front_base + f) + c - C.front_base;
+      kc[c] = child_at0 ? 0 : C.pat[(size_t)C.pattern_of[chs[c]] * TF_PAT_WIDTH + TF_PAT_K];
+    }
+    const int* inv = L.maps + s.ioff;
+    for (int r = tid; r < m; r += 256) {
+      double v = r < k ? y[(piv + r) * ldr + col0] : 0.0;
+      for (int c = 0; c < s.nsrc; c++) {
+        const int i = __ldg(inv + c * m + r);
+        if (i >= 0) v += w_child[(chs[c] * child_rows + kc[c] + i) * ldr + col0];
+      }
+      W[r] = v;
+    }
+  }
+  __syncthreads();
+  const int t0 = (lane & 7) * 8;
+  const int gr = (lane >> 3) + 4 * (lane & 7);
+  for (int b = 0; b < nb; b++) {
+    const int c0 = b * TB, kb = min(TB, k - c0);
+    double vt[8];
+    double yv = 0.0;
+    const int n = 32 * warp + gr;
+    if (warp < 2 && 32 * warp < kb) {
+#pragma unroll
+      for (int h = 0; h < 8; h++) vt[h] = t0 + h < kb ? W[c0 + t0 + h] : 0.0;
+      const double* M = L.aux + f * L.aux_stride + (long long)b * TB * TB;
+      const double red = rows32_dot<8, true>(M, TB, 32 * warp, kb, kb, vt);
+      if (n < kb) yv = W[c0 + n] + red;
+    }
+    __syncthreads();
+    if (warp < 2 && n < kb) {
+      W[c0 + n] = yv;
+      y[(piv + c0 + n) * ldr + col0] = yv / Pf[(long long)m * kp + c0 + n];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 8; h++) vt[h] = t0 + h < kb ? W[c0 + t0 + h] : 0.0;
+    for (int rs = c0 + kb + 32 * warp; rs < m; rs += 256) {
+      const double red = rows32_dot<8, false>(Pf + c0, kp, rs, m, kb, vt);
+      const int r = rs + gr;
+      if (r < m) W[r] -= red;
+    }
+    __syncthreads();
+  }
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int r = k + tid; r < m; r += 256) out[(long long)r * ldr] = W[r];
+}
+
+__global__ void __launch_bounds__(256)
+    solve_bwd_front(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
+                    const double* __restrict__ x_parent, long long parent_rows, double* x_out,
+                    long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double fsm[];
+  double* red = fsm;            // [8][TB]
+  double* Z = red + 8 * TB;     // [TB]
+  double* X = Z + TB;           // [max_m]
+  const long long f = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  const int* mp = nullptr;
+  const double* Xp = nullptr;
+  if (has_parent && m > k) {
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
+    mp = PA.maps + (((L.front_base + f) & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    Xp = x_parent + pf * parent_rows * ldr + col0;
+  }
+  for (int r = tid; r < m; r += 256)
+    X[r] = r < k ? y[(piv + r) * ldr + col0] : (mp ? Xp[(long long)__ldg(mp + r - k) * ldr] : 0.0);
+  __syncthreads();
+  for (int b = nb - 1; b >= 0; b--) {
+    const int c0 = b * TB, kb = min(TB, k - c0);
+    // z_b = X_b - sum over the rows below of l_rc x_r
+    double acc[2] = {0.0, 0.0};
+    const double* Pc = Pf + c0;
+    int r = c0 + kb + warp;
+    for (; r + 24 < m; r += 32) {  // four rows of this warp in flight
+      double lv[4][2], xr[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        xr[u] = X[r + 8 * u];
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const int c = lane + 32 * q;
+          lv[u][q] = c < kb ? __ldg(Pc + (long long)(r + 8 * u) * kp + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int q = 0; q < 2; q++) acc[q] += lv[u][q] * xr[u];
+    }
+    for (; r < m; r += 8) {
+      const double xr = X[r];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int c = lane + 32 * q;
+        if (c < kb) acc[q] += __ldg(Pc + (long long)r * kp + c) * xr;
+      }
+    }
+    red[warp * TB + lane] = acc[0];
+    red[warp * TB + lane + 32] = acc[1];
+    __syncthreads();
+    if (tid < kb) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; w++) t += red[w * TB + tid];
+      Z[tid] = X[c0 + tid] - t;
+    }
+    __syncthreads();
+    // X_b = M_b^T z_b: x_c = z_c + sum_{n > c} M(n, c) z_n
+    const double* M = L.aux + f * L.aux_stride + (long long)b * TB * TB;
+    acc[0] = acc[1] = 0.0;
+    for (int n = warp; n < kb; n += 8) {
+      const double zn = Z[n];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int c = lane + 32 * q;
+        if (c < n) acc[q] += __ldg(M + n * TB + c) * zn;
+      }
+    }
+    red[warp * TB + lane] = acc[0];
+    red[warp * TB + lane + 32] = acc[1];
+    __syncthreads();
+    if (tid < kb) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; w++) t += red[w * TB + tid];
+      const double xv = Z[tid] + t;
+      X[c0 + tid] = xv;
+      y[(piv + c0 + tid) * ldr + col0] = xv;
+    }
+    __syncthreads();
+  }
+  double* Xo = x_out + f * out_rows * ldr + col0;
+  for (int rr = tid; rr < m; rr += 256) Xo[(long long)rr * ldr] = X[rr];
+}
+
+// Measured on cfg5 (k = 128, 256): the backward CTA-per-front sweep beats
+// the wavefront kernel from 512 fronts up (2.1-2.5x); the forward one is
+// slower than the wavefront at every level, so it is off unless forced
+// (TFB_FRONT_SOLVE=2; 0 disables both).
+static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_FRONT_SOLVE");
+    v = e ? atoi(e) : 1;
+  }
+  static long long min_fronts = -1;  // TFB_FRONT_MIN_FRONTS (tests: drive small meshes through it)
+  if (min_fronts < 0) {
+    const char* e = getenv("TFB_FRONT_MIN_FRONTS");
+    min_fronts = e ? atoll(e) : 0;
+  }
+  if (v == 0 || (fwd && v < 2)) return false;
+  const long long need = min_fronts > 0 ? min_fronts : (fwd ? 128 : 512);
+  return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= need &&
+         (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
+}
+
 static bool narrow_solve(const LevelArgs& L, int nrhs) {
   static int v = -1;  // TFB_NARROW_SOLVE=0: wavefront kernels instead (A/B)
   if (v < 0) {
@@ -1079,6 +1267,15 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
     timer_end(st);
     return cudaGetLastError();
   }
+  if (front_solve(L, nrhs, true)) {
+    const size_t smem = (size_t)L.max_m * 8;
+    narrow_attr(solve_fwd_front, smem);
+    timer_begin(K_SOLVE_FWD_WAVE, st);
+    solve_fwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(L, C, child_at0, factors, w_child,
+                                                             child_rows, w_out, out_rows, y, nrhs, 0);
+    timer_end(st);
+    return cudaGetLastError();
+  }
   if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const int nb = (L.max_k + TB - 1) / TB, rt = (L.max_m + TB - 1) / TB;
   const int cw = std::min(nrhs, kWaveCols);
@@ -1129,6 +1326,15 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
     timer_end(st);
     return cudaGetLastError();
   }
+  if (front_solve(L, nrhs, false)) {
+    const size_t smem = (size_t)(L.max_m + 9 * TB) * 8;
+    narrow_attr(solve_bwd_front, smem);
+    timer_begin(K_SOLVE_BWD_WAVE, st);
+    solve_bwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(L, PA, has_parent, factors, x_parent,
+                                                             parent_rows, x_out, out_rows, y, nrhs, 0);
+    timer_end(st);
+    return cudaGetLastError();
+  }
   if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
   const unsigned nf = (unsigned)L.n_fronts;
   const long long nW = (long long)L.max_m * nrhs;
@@ -1165,7 +1371,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   if (!level_is_large(L.is_leaf, L.max_m)) return (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
-  if (narrow_solve(L, nrhs)) return 1;
+  if (narrow_solve(L, nrhs) || front_solve(L, nrhs, fwd)) return 1;
   const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
   if (fwd) return slices;
   return 1 + (L.max_k > 0 ? slices : 0);

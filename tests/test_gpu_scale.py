@@ -53,3 +53,52 @@ def test_against_c_oracle_large_path(limit):
     assert np.array_equal(o.arrays()["pivot_order"], plan.pivot_order_array)
     xr = o.solve(b)
     assert np.abs(x - xr).max() / np.abs(xr).max() <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,p", [((512, 512), 1), ((1024, 1024), 1), ((128, 128), 2), ((16, 16, 16), 1)])
+def test_single_rhs_at_scale(shape, p, limit):
+    """One right-hand side takes the single-column kernels (warp-per-front and
+    CTA-per-front sweeps on large levels, in-place panel reads on small ones)."""
+    mesh, fronts, system, plan = pipeline(shape, p)
+    f = tf.run_sequential(plan, tf.init_state(system, plan))
+    b = np.random.default_rng(11).standard_normal(mesh.n_dof)
+    x = tf.solve(f, b)
+    assert np.abs(system.matvec(x) - b).max() / np.abs(b).max() < 1e-12
+    assert np.array_equal(tf.solve(f, b), x)
+
+
+_FORCED_SWEEPS = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2306_08994_b200 as tf
+from paper_2306_08994_b200 import device
+device.set_small_front_limit({limit})
+mesh = tf.TensorMesh({shape!r}, 1)
+fronts = tf.generate_fronts(mesh)
+tree = tf.build_elimination_tree(tf.sort_fronts(fronts), n_dof=mesh.n_dof)
+system = tf.assemble_system(mesh, "one")
+plan = tf.symbolic_eliminate(tree, system)
+f = tf.run_sequential(plan, tf.init_state(system, plan))
+b = np.random.default_rng(13).standard_normal(mesh.n_dof)
+x = tf.solve(f, b)
+res = np.abs(system.matvec(x) - b).max() / np.abs(b).max()
+assert res < 1e-12, res
+assert np.array_equal(tf.solve(f, b), x)
+print("ok", res)
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,limit", [((512, 512), 112), ((256, 256), 1), ((16, 16, 16), 1)])
+def test_forced_front_sweeps(shape, limit, cuda_ok):
+    """The CTA-per-front forward and backward sweeps on every large level with
+    k > 64 (thresholds lowered through the environment, fresh process)."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, TFB_FRONT_SOLVE="2", TFB_FRONT_MIN_FRONTS="1")
+    out = subprocess.run([sys.executable, "-c", _FORCED_SWEEPS.format(root=root, shape=shape, limit=limit)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.startswith("ok")
