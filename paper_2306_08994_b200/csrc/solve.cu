@@ -712,25 +712,36 @@ constexpr int kNarrowWarps = 8;
 // Returns the sum for row r0 + g + 4c (lane (g, c)).
 template <int CW, bool TRI>
 __device__ __forceinline__ double rows32_dot(const double* __restrict__ A, int lda, int r0,
-                                             int rend, int k, const double (&vt)[CW]) {
+                                             int rend, int k, const double (&vt)[CW],
+                                             int ncol) {  // readable columns of A's rows (even)
   const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7, t0 = c * CW;
+  // branch-free: every load is issued up front (rows clamped into the block,
+  // columns past the limit read in-bounds neighbours and are masked to zero)
+  // (in two halves of four rows: 16-32 registers of loads in flight)
   double v[8];
 #pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const int r = r0 + g + 4 * j;
-    const int lim = TRI ? min(k, r) : k;
-    double p = 0.0;
-    if (r < rend) {
+  for (int hf = 0; hf < 8; hf += 4) {
+    double2 x[4][CW / 2];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int r = min(r0 + g + 4 * (hf + j), rend - 1);
+#pragma unroll
+      for (int h = 0; h < CW; h += 2)
+        x[j][h / 2] = __ldg(reinterpret_cast<const double2*>(A + (long long)r * lda +
+                                                              min(t0 + h, ncol - 2)));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int r = r0 + g + 4 * (hf + j);
+      const int lim = r < rend ? (TRI ? min(k, r) : k) : 0;
+      double p = 0.0;
 #pragma unroll
       for (int h = 0; h < CW; h += 2) {
-        if (t0 + h < lim) {
-          const double2 x = __ldg(reinterpret_cast<const double2*>(A + (long long)r * lda + t0 + h));
-          p += x.x * vt[h];
-          if (t0 + h + 1 < lim) p += x.y * vt[h + 1];
-        }
+        p = fma(t0 + h < lim ? x[j][h / 2].x : 0.0, vt[h], p);
+        p = fma(t0 + h + 1 < lim ? x[j][h / 2].y : 0.0, vt[h + 1], p);
       }
+      v[hf + j] = p;
     }
-    v[j] = p;
   }
 #pragma unroll
   for (int off = 4; off >= 1; off >>= 1) {
@@ -747,7 +758,7 @@ __device__ __forceinline__ double rows32_dot(const double* __restrict__ A, int l
 
 // CW = panel columns per lane (8 lanes per row): 4 for k <= 32, 8 for k <= 64
 template <int CW>
-__global__ void __launch_bounds__(32 * kNarrowWarps)
+__global__ void __launch_bounds__(32 * kNarrowWarps, 4)
     solve_fwd_narrow(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
                      const double* __restrict__ w_child, long long child_rows, double* w_out,
                      long long out_rows, double* y, int ldr, int col0) {
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(32 * kNarrowWarps)
   for (int b = 0; b < 2; b++) {
     yv[b] = 0.0;
     if (32 * b < k) {
-      const double red = rows32_dot<CW, true>(M, TB, 32 * b, k, k, vt);
+      const double red = rows32_dot<CW, true>(M, TB, 32 * b, k, k, vt, TB);
       const int n = 32 * b + gr;
       if (n < k) yv[b] = W[n] + red;
     }
@@ -811,7 +822,7 @@ __global__ void __launch_bounds__(32 * kNarrowWarps)
   for (int h = 0; h < CW; h++) vt[h] = t0 + h < k ? W[t0 + h] : 0.0;
   double* out = w_out + f * out_rows * ldr + col0;
   for (int r0 = k; r0 < m; r0 += 32) {
-    const double red = rows32_dot<CW, false>(Pf, kp, r0, m, k, vt);
+    const double red = rows32_dot<CW, false>(Pf, kp, r0, m, k, vt, kp);
     const int r = r0 + gr;
     if (r < m) out[(long long)r * ldr] = W[r] - red;
   }
@@ -959,7 +970,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int h = 0; h < 8; h++) vt[h] = t0 + h < kb ? W[c0 + t0 + h] : 0.0;
       const double* M = L.aux + f * L.aux_stride + (long long)b * TB * TB;
-      const double red = rows32_dot<8, true>(M, TB, 32 * warp, kb, kb, vt);
+      const double red = rows32_dot<8, true>(M, TB, 32 * warp, kb, kb, vt, TB);
       if (n < kb) yv = W[c0 + n] + red;
     }
     __syncthreads();
@@ -971,7 +982,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int h = 0; h < 8; h++) vt[h] = t0 + h < kb ? W[c0 + t0 + h] : 0.0;
     for (int rs = c0 + kb + 32 * warp; rs < m; rs += 256) {
-      const double red = rows32_dot<8, false>(Pf + c0, kp, rs, m, kb, vt);
+      const double red = rows32_dot<8, false>(Pf + c0, kp, rs, m, kb, vt, kp - c0);
       const int r = rs + gr;
       if (r < m) W[r] -= red;
     }
@@ -1075,9 +1086,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // Measured on cfg5 (k = 128, 256): the backward CTA-per-front sweep beats
-// the wavefront kernel from 512 fronts up (2.1-2.5x); the forward one is
-// slower than the wavefront at every level, so it is off unless forced
-// (TFB_FRONT_SOLVE=2; 0 disables both).
+// the wavefront kernel from 512 fronts up (2.1-2.5x), the forward one from
+// 256 fronts up (5-15%); below that the wavefront's tile parallelism wins
+// (TFB_FRONT_SOLVE=0 disables both; TFB_FRONT_MIN_FRONTS overrides the bound).
 static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
   static int v = -1;
   if (v < 0) {
@@ -1089,8 +1100,8 @@ static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
     const char* e = getenv("TFB_FRONT_MIN_FRONTS");
     min_fronts = e ? atoll(e) : 0;
   }
-  if (v == 0 || (fwd && v < 2)) return false;
-  const long long need = min_fronts > 0 ? min_fronts : (fwd ? 128 : 512);
+  if (v == 0) return false;
+  const long long need = min_fronts > 0 ? min_fronts : (fwd ? 256 : 512);
   return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= need &&
          (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
