@@ -1023,10 +1023,10 @@ __global__ void __launch_bounds__(256)
     double acc[2] = {0.0, 0.0};
     const double* Pc = Pf + c0;
     int r = c0 + kb + warp;
-    for (; r + 24 < m; r += 32) {  // four rows of this warp in flight
-      double lv[4][2], xr[4];
+    for (; r + 56 < m; r += 64) {  // eight rows of this warp in flight
+      double lv[8][2], xr[8];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < 8; u++) {
         xr[u] = X[r + 8 * u];
 #pragma unroll
         for (int q = 0; q < 2; q++) {
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(256)
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++)
+      for (int u = 0; u < 8; u++)
 #pragma unroll
         for (int q = 0; q < 2; q++) acc[q] += lv[u][q] * xr[u];
     }
@@ -1085,9 +1085,9 @@ __global__ void __launch_bounds__(256)
   for (int rr = tid; rr < m; rr += 256) Xo[(long long)rr * ldr] = X[rr];
 }
 
-// Measured on cfg5 (k = 128, 256): the backward CTA-per-front sweep beats
-// the wavefront kernel from 512 fronts up (2.1-2.5x), the forward one from
-// 256 fronts up (5-15%); below that the wavefront's tile parallelism wins
+// Measured on cfg5 (k = 128, 256): the CTA-per-front sweeps beat the
+// wavefront kernels from 256 fronts up (backward 1.2-2.5x, forward 5-15%);
+// below that the wavefront's tile parallelism wins
 // (TFB_FRONT_SOLVE=0 disables both; TFB_FRONT_MIN_FRONTS overrides the bound).
 static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
   static int v = -1;
@@ -1101,7 +1101,7 @@ static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
     min_fronts = e ? atoll(e) : 0;
   }
   if (v == 0) return false;
-  const long long need = min_fronts > 0 ? min_fronts : (fwd ? 256 : 512);
+  const long long need = min_fronts > 0 ? min_fronts : 256;
   return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= need &&
          (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
