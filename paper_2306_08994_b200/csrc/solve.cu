@@ -1089,6 +1089,136 @@ __global__ void __launch_bounds__(256)
 // wavefront kernels from 256 fronts up (backward 1.2-2.5x, forward 5-15%);
 // below that the wavefront's tile parallelism wins
 // (TFB_FRONT_SOLVE=0 disables both; TFB_FRONT_MIN_FRONTS overrides the bound).
+// ----------------------------------------- small fronts, one RHS, 8 < k <= 16
+// A warp per front (non-leaf small levels): the pivot triangle by warp
+// substitution (each lane holds its row / column of L11 in registers,
+// pivots broadcast by shuffles), the update rows by rows32_dot (eight lanes
+// per 128-byte panel row) forward, and by column accumulation over two row
+// streams backward.  Block conventions as solve_fwd_small / solve_bwd_small.
+constexpr int kSmallWarps = 8;
+
+__global__ void __launch_bounds__(32 * kSmallWarps)
+    solve_fwd_warp16(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
+                     const double* __restrict__ w_child, long long child_rows, int child_at0,
+                     double* w_out, long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double wsm16[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kSmallWarps + warp;
+  if (f >= L.n_fronts) return;
+  double* W = wsm16 + (long long)warp * L.max_m;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  for (int r = lane; r < m; r += 32) W[r] = r < k ? y[(piv + r) * ldr + col0] : 0.0;
+  __syncwarp();
+  for (int c = 0; c < s.nsrc; c++) {  // children one after the other (shared rows collide)
+    const long long ch = 2 * (L.front_base + f) + c - C.front_base;
+    const int off = child_at0 ? 0 : C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
+    const int len = c == 0 ? s.len0 : s.len1;
+    const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
+    const double* Wc = w_child + (ch * child_rows + off) * ldr + col0;
+    for (int a = lane; a < len; a += 32) W[__ldg(mp + a)] += Wc[(long long)a * ldr];
+    __syncwarp();
+  }
+  // pivot triangle: lane r < k holds w_r and row r of L11
+  double lr[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) lr[j] = (lane < k && j < lane) ? __ldg(Pf + (long long)lane * kp + j) : 0.0;
+  double w = lane < k ? W[lane] : 0.0;
+#pragma unroll
+  for (int c = 0; c < 15; c++) {
+    const double yc = __shfl_sync(0xffffffffu, w, c);
+    w -= lr[c] * yc;  // lr[c] = 0 unless c < lane < k
+  }
+  if (lane < k) {
+    W[lane] = w;
+    y[(piv + lane) * ldr + col0] = w / Pf[(long long)m * kp + lane];
+  }
+  __syncwarp();
+  const int t0 = (lane & 7) * 2;
+  const int gr = (lane >> 3) + 4 * (lane & 7);
+  double vt[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) vt[h] = t0 + h < k ? W[t0 + h] : 0.0;
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int r0 = k; r0 < m; r0 += 32) {
+    const double red = rows32_dot<2, false>(Pf, kp, r0, m, k, vt, kp);
+    const int r = r0 + gr;
+    if (r < m) out[(long long)(r - k) * ldr] = W[r] - red;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kSmallWarps)
+    solve_bwd_warp16(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
+                     const double* __restrict__ x_parent, long long parent_rows, double* x_out,
+                     long long out_rows, double* y, int ldr, int col0) {
+  extern __shared__ __align__(16) double wsm16[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kSmallWarps + warp;
+  if (f >= L.n_fronts) return;
+  double* X = wsm16 + (long long)warp * L.max_m;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pf = factors + f * L.fac_stride;
+  const int* mp = nullptr;
+  const double* Xp = nullptr;
+  if (has_parent && m > k) {
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
+    mp = PA.maps + (((L.front_base + f) & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    Xp = x_parent + pf * parent_rows * ldr + col0;
+  }
+  for (int r = lane; r < m; r += 32)
+    X[r] = r < k ? y[(piv + r) * ldr + col0] : (mp ? Xp[(long long)__ldg(mp + r - k) * ldr] : 0.0);
+  __syncwarp();
+  // z_c = y_c - sum_{r >= k} l_rc x_r: lane (half, c) = (lane / 16, lane % 16), rows by parity
+  const int c = lane & 15, hr = lane >> 4;
+  double acc = 0.0;
+  int r = k + hr;
+  for (; r + 6 < m; r += 8) {  // four rows of this half in flight
+    double lv[4], xr[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      lv[u] = c < k ? __ldg(Pf + (long long)(r + 2 * u) * kp + c) : 0.0;
+      xr[u] = X[r + 2 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) acc += lv[u] * xr[u];
+  }
+  for (; r < m; r += 2) acc += (c < k ? __ldg(Pf + (long long)r * kp + c) : 0.0) * X[r];
+  acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+  // backward substitution with L11^T: lane c < k holds column c of L11
+  double lc[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) lc[j] = (lane < k && j > lane && j < k) ? __ldg(Pf + (long long)j * kp + lane) : 0.0;
+  double z = lane < k ? X[lane] - acc : 0.0;
+#pragma unroll
+  for (int j = 15; j > 0; j--) {
+    const double xj = __shfl_sync(0xffffffffu, z, j);
+    z -= lc[j] * xj;  // lc[j] = 0 unless lane < j < k
+  }
+  __syncwarp();
+  if (lane < k) {
+    y[(piv + lane) * ldr + col0] = z;
+    X[lane] = z;
+  }
+  __syncwarp();
+  double* Xo = x_out + f * out_rows * ldr + col0;
+  for (int rr = lane; rr < m; rr += 32) Xo[(long long)rr * ldr] = X[rr];
+}
+
+static bool warp16_solve(const LevelArgs& L, int nrhs) {
+  static int v = -1;  // TFB_WARP16_SOLVE=0: group-per-front kernels instead (A/B)
+  if (v < 0) {
+    const char* e = getenv("TFB_WARP16_SOLVE");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  // measured on cfg5: 2x faster at k = 16 (m = 79, 111), 1.4x slower at k = 8
+  return v && nrhs == 1 && !L.is_leaf && L.max_k > 8 && L.max_k <= 16;
+}
+
 static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
   static int v = -1;
   if (v < 0) {
@@ -1166,6 +1296,21 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
                                   const double* factors, const double* w_in, long long in_rows,
                                   double* w_out, long long out_rows, double* y, int nrhs,
                                   cudaStream_t st) {
+  if (warp16_solve(L, nrhs)) {
+    const size_t smem = (size_t)kSmallWarps * L.max_m * 8;
+    const unsigned g = (unsigned)((L.n_fronts + kSmallWarps - 1) / kSmallWarps);
+    if (FWD) {
+      timer_begin(K_SOLVE_SMALL_FWD, st);
+      solve_fwd_warp16<<<g, 32 * kSmallWarps, smem, st>>>(L, O, factors, w_in, in_rows, flag, w_out,
+                                                          out_rows, y, nrhs, 0);
+    } else {
+      timer_begin(K_SOLVE_SMALL_BWD, st);
+      solve_bwd_warp16<<<g, 32 * kSmallWarps, smem, st>>>(L, O, flag, factors, w_in, in_rows, w_out,
+                                                          out_rows, y, nrhs, 0);
+    }
+    timer_end(st);
+    return cudaGetLastError();
+  }
   const int cw = small_cols(L, nrhs);
   if (FWD && L.is_leaf) {  // fronts without pivots leave zero update blocks
     cudaError_t e = cudaMemsetAsync(w_out, 0, sizeof(double) * (size_t)L.n_fronts * out_rows * nrhs, st);
@@ -1381,7 +1526,8 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 }
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
-  if (!level_is_large(L.is_leaf, L.max_m)) return (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
+  if (!level_is_large(L.is_leaf, L.max_m))
+    return warp16_solve(L, nrhs) ? 1 : (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
   if (narrow_solve(L, nrhs) || front_solve(L, nrhs, fwd)) return 1;
   const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
   if (fwd) return slices;
