@@ -932,13 +932,17 @@ __global__ void __launch_bounds__(32 * kNarrowWarps)
 __global__ void __launch_bounds__(256)
     solve_fwd_front(LevelArgs L, LevelArgs C, int child_at0, const double* __restrict__ factors,
                     const double* __restrict__ w_child, long long child_rows, double* w_out,
-                    long long out_rows, double* y, int ldr, int col0) {
+                    long long out_rows, double* y, int ldr, int col0, double* ywork, int kcols) {
+  // ywork != nullptr (split mode): pivot rows only; the unscaled Y goes to
+  // ywork[f * kcols + t] for solve_fwd_split_rows, which owns the update rows
   extern __shared__ __align__(16) double fsm[];
   double* W = fsm;
   const long long f = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Shape s = front_shape(L, f);
-  const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const int k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const int m = ywork ? k : s.m;  // rows this kernel sweeps
+  const int mf = s.m;             // the panel's row count (d follows it)
   const long long piv = L.piv_off[f];
   const double* Pf = factors + f * L.fac_stride;
   {
@@ -952,7 +956,7 @@ __global__ void __launch_bounds__(256)
     for (int r = tid; r < m; r += 256) {
       double v = r < k ? y[(piv + r) * ldr + col0] : 0.0;
       for (int c = 0; c < s.nsrc; c++) {
-        const int i = __ldg(inv + c * m + r);
+        const int i = __ldg(inv + c * mf + r);
         if (i >= 0) v += w_child[(chs[c] * child_rows + kc[c] + i) * ldr + col0];
       }
       W[r] = v;
@@ -976,7 +980,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (warp < 2 && n < kb) {
       W[c0 + n] = yv;
-      y[(piv + c0 + n) * ldr + col0] = yv / Pf[(long long)m * kp + c0 + n];
+      y[(piv + c0 + n) * ldr + col0] = yv / Pf[(long long)mf * kp + c0 + n];
     }
     __syncthreads();
 #pragma unroll
@@ -988,14 +992,78 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
   }
+  if (ywork) {
+    for (int t = tid; t < k; t += 256) ywork[f * kcols + t] = W[t];
+    return;
+  }
   double* out = w_out + f * out_rows * ldr + col0;
   for (int r = k + tid; r < m; r += 256) out[(long long)r * ldr] = W[r];
+}
+
+// Split forward sweep, update rows: grid (fronts, chunks of kSplitRows rows of
+// [k, m)); W_r (children gathered) - sum over the 64-column blocks of
+// L[r, b] Y_b, Y from solve_fwd_front's split mode.
+constexpr int kSplitRows = 256;
+__global__ void __launch_bounds__(256)
+    solve_fwd_split_rows(LevelArgs L, LevelArgs C, int child_at0,
+                         const double* __restrict__ factors, const double* __restrict__ w_child,
+                         long long child_rows, double* w_out, long long out_rows,
+                         const double* __restrict__ ywork, int kcols, int ldr, int col0) {
+  extern __shared__ __align__(16) double fsm[];
+  double* W = fsm;              // [kSplitRows]
+  double* Ys = W + kSplitRows;  // [kcols]
+  const long long f = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const int rs = k + blockIdx.y * kSplitRows;
+  if (rs >= m) return;
+  const int re = min(m, rs + kSplitRows);
+  const double* Pf = factors + f * L.fac_stride;
+  {
+    long long chs[2] = {0, 0};
+    int kc[2] = {0, 0};
+    for (int c = 0; c < s.nsrc; c++) {
+      chs[c] = 2 * (L.front_base + f) + c - C.front_base;
+      kc[c] = child_at0 ? 0 : C.pat[(size_t)C.pattern_of[chs[c]] * TF_PAT_WIDTH + TF_PAT_K];
+    }
+    const int* inv = L.maps + s.ioff;
+    for (int r = rs + tid; r < re; r += 256) {
+      double v = 0.0;
+      for (int c = 0; c < s.nsrc; c++) {
+        const int i = __ldg(inv + c * m + r);
+        if (i >= 0) v += w_child[(chs[c] * child_rows + kc[c] + i) * ldr + col0];
+      }
+      W[r - rs] = v;
+    }
+  }
+  for (int t = tid; t < k; t += 256) Ys[t] = __ldcg(ywork + f * kcols + t);
+  __syncthreads();
+  const int t0 = (lane & 7) * 8;
+  const int gr = (lane >> 3) + 4 * (lane & 7);
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int r0 = rs + 32 * warp; r0 < re; r0 += 256) {
+    double red = 0.0;
+    for (int b = 0; b < nb; b++) {
+      const int c0 = b * TB, kb = min(TB, k - c0);
+      double vt[8];
+#pragma unroll
+      for (int h = 0; h < 8; h++) vt[h] = t0 + h < kb ? Ys[c0 + t0 + h] : 0.0;
+      red += rows32_dot<8, false>(Pf + c0, kp, r0, re, kb, vt, kp - c0);
+    }
+    const int r = r0 + gr;
+    if (r < re) out[(long long)r * ldr] = W[r - rs] - red;
+  }
 }
 
 __global__ void __launch_bounds__(256)
     solve_bwd_front(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
                     const double* __restrict__ x_parent, long long parent_rows, double* x_out,
-                    long long out_rows, double* y, int ldr, int col0) {
+                    long long out_rows, double* y, int ldr, int col0, const double* part,
+                    int nchunk, int kcols) {
+  // part != nullptr (split mode): the update rows' contributions were summed
+  // per chunk by solve_bwd_split_rows (part[(f * nchunk + chunk) * kcols + c]);
+  // this kernel sweeps the pivot rows only
   extern __shared__ __align__(16) double fsm[];
   double* red = fsm;            // [8][TB]
   double* Z = red + 8 * TB;     // [TB]
@@ -1003,7 +1071,9 @@ __global__ void __launch_bounds__(256)
   const long long f = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Shape s = front_shape(L, f);
-  const int m = s.m, k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const int k = s.k, kp = s.kp, nb = (k + TB - 1) / TB;
+  const int m = part ? k : s.m;
+  const int nch = part ? (s.m - k + kSplitRows - 1) / kSplitRows : 0;
   const long long piv = L.piv_off[f];
   const double* Pf = factors + f * L.fac_stride;
   const int* mp = nullptr;
@@ -1054,6 +1124,7 @@ __global__ void __launch_bounds__(256)
       double t = 0.0;
 #pragma unroll
       for (int w = 0; w < 8; w++) t += red[w * TB + tid];
+      for (int ch = 0; ch < nch; ch++) t += __ldcg(part + (f * nchunk + ch) * kcols + c0 + tid);
       Z[tid] = X[c0 + tid] - t;
     }
     __syncthreads();
@@ -1217,6 +1288,93 @@ static bool warp16_solve(const LevelArgs& L, int nrhs) {
   }
   // measured on cfg5: 2x faster at k = 16 (m = 79, 111), 1.4x slower at k = 8
   return v && nrhs == 1 && !L.is_leaf && L.max_k > 8 && L.max_k <= 16;
+}
+
+// Split backward sweep, update rows: grid (fronts, chunks of kSplitRows rows,
+// 64-column blocks); partial z of the chunk for the block's columns (warps
+// split the rows, lanes own columns, fixed-order combine).  Block 0 of each
+// chunk also writes the chunk's rows of the front's X block for the children.
+__global__ void __launch_bounds__(256)
+    solve_bwd_split_rows(LevelArgs L, LevelArgs PA, int has_parent,
+                         const double* __restrict__ factors, const double* __restrict__ x_parent,
+                         long long parent_rows, double* x_out, long long out_rows, double* part,
+                         int nchunk, int kcols, int ldr, int col0) {
+  __shared__ double Xs[kSplitRows];
+  __shared__ double red[8][TB];
+  const long long f = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const int rs = k + blockIdx.y * kSplitRows, c0 = blockIdx.z * TB;
+  if (rs >= m || c0 >= k) return;
+  const int re = min(m, rs + kSplitRows), kb = min(TB, k - c0);
+  const double* Pf = factors + f * L.fac_stride;
+  if (has_parent) {
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
+    const int* mp = PA.maps + (((L.front_base + f) & 1) == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    const double* Xp = x_parent + pf * parent_rows * ldr + col0;
+    for (int r = rs + tid; r < re; r += 256) Xs[r - rs] = Xp[(long long)__ldg(mp + r - k) * ldr];
+  } else {
+    for (int r = rs + tid; r < re; r += 256) Xs[r - rs] = 0.0;
+  }
+  __syncthreads();
+  if (blockIdx.z == 0) {
+    double* Xo = x_out + f * out_rows * ldr + col0;
+    for (int r = rs + tid; r < re; r += 256) Xo[(long long)r * ldr] = Xs[r - rs];
+  }
+  double acc[2] = {0.0, 0.0};
+  const double* Pc = Pf + c0;
+  int r = rs + warp;
+  for (; r + 56 < re; r += 64) {  // eight rows of this warp in flight
+    double lv[8][2], xr[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      xr[u] = Xs[r + 8 * u - rs];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int c = lane + 32 * q;
+        lv[u][q] = c < kb ? __ldg(Pc + (long long)(r + 8 * u) * kp + c) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+#pragma unroll
+      for (int q = 0; q < 2; q++) acc[q] += lv[u][q] * xr[u];
+  }
+  for (; r < re; r += 8) {
+    const double xr = Xs[r - rs];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      const int c = lane + 32 * q;
+      if (c < kb) acc[q] += __ldg(Pc + (long long)r * kp + c) * xr;
+    }
+  }
+  red[warp][lane] = acc[0];
+  red[warp][lane + 32] = acc[1];
+  __syncthreads();
+  if (tid < kb) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) t += red[w][tid];
+    part[(f * nchunk + blockIdx.y) * kcols + c0 + tid] = t;
+  }
+}
+
+// Levels with fewer fronts (k > 64): split sweeps, the update rows spread
+// over (front, row chunk) CTAs.  Measured on cfg5: backward 1.4-2x faster
+// than the wavefront from 32 fronts up; forward slower at every level (its
+// pivot-row pass is one CTA per front), so it runs only when forced.
+// TFB_SPLIT_SOLVE=0: off; 2: both directions on every such level (tests).
+static bool split_solve(const LevelArgs& L, int nrhs, bool fwd) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_SPLIT_SOLVE");
+    v = e ? atoi(e) : 1;
+  }
+  if (v == 0 || (fwd && v < 2)) return false;
+  return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= (v >= 2 ? 1 : 32) &&
+         (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
 
 static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
@@ -1427,8 +1585,24 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
     const size_t smem = (size_t)L.max_m * 8;
     narrow_attr(solve_fwd_front, smem);
     timer_begin(K_SOLVE_FWD_WAVE, st);
-    solve_fwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(L, C, child_at0, factors, w_child,
-                                                             child_rows, w_out, out_rows, y, nrhs, 0);
+    solve_fwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(
+        L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, y, nrhs, 0, nullptr, 0);
+    timer_end(st);
+    return cudaGetLastError();
+  }
+  if (split_solve(L, nrhs, true)) {
+    if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
+    const int kcols = (L.max_k + TB - 1) / TB * TB;
+    const unsigned nch = (unsigned)std::max(1, (L.max_upd + kSplitRows - 1) / kSplitRows);
+    const size_t smem = (size_t)L.max_m * 8;
+    narrow_attr(solve_fwd_front, smem);
+    timer_begin(K_SOLVE_FWD_WAVE, st);
+    solve_fwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(
+        L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, y, nrhs, 0, work, kcols);
+    const size_t smem2 = (size_t)(kSplitRows + kcols) * 8;
+    narrow_attr(solve_fwd_split_rows, smem2);
+    solve_fwd_split_rows<<<dim3((unsigned)L.n_fronts, nch), 256, smem2, st>>>(
+        L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, work, kcols, nrhs, 0);
     timer_end(st);
     return cudaGetLastError();
   }
@@ -1486,8 +1660,23 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
     const size_t smem = (size_t)(L.max_m + 9 * TB) * 8;
     narrow_attr(solve_bwd_front, smem);
     timer_begin(K_SOLVE_BWD_WAVE, st);
-    solve_bwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(L, PA, has_parent, factors, x_parent,
-                                                             parent_rows, x_out, out_rows, y, nrhs, 0);
+    solve_bwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(
+        L, PA, has_parent, factors, x_parent, parent_rows, x_out, out_rows, y, nrhs, 0, nullptr, 0, 0);
+    timer_end(st);
+    return cudaGetLastError();
+  }
+  if (split_solve(L, nrhs, false)) {
+    if (!work || work_doubles < solve_workspace_doubles(L, nrhs)) return cudaErrorInvalidValue;
+    const int kcols = (L.max_k + TB - 1) / TB * TB;
+    const int nch = std::max(1, (L.max_upd + kSplitRows - 1) / kSplitRows);
+    timer_begin(K_SOLVE_BWD_WAVE, st);
+    if (L.max_upd > 0)
+      solve_bwd_split_rows<<<dim3((unsigned)L.n_fronts, (unsigned)nch, (unsigned)(kcols / TB)), 256, 0, st>>>(
+          L, PA, has_parent, factors, x_parent, parent_rows, x_out, out_rows, work, nch, kcols, nrhs, 0);
+    const size_t smem = (size_t)(L.max_m + 9 * TB) * 8;
+    narrow_attr(solve_bwd_front, smem);
+    solve_bwd_front<<<(unsigned)L.n_fronts, 256, smem, st>>>(
+        L, PA, has_parent, factors, x_parent, parent_rows, x_out, out_rows, y, nrhs, 0, work, nch, kcols);
     timer_end(st);
     return cudaGetLastError();
   }
@@ -1529,6 +1718,7 @@ int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   if (!level_is_large(L.is_leaf, L.max_m))
     return warp16_solve(L, nrhs) ? 1 : (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
   if (narrow_solve(L, nrhs) || front_solve(L, nrhs, fwd)) return 1;
+  if (split_solve(L, nrhs, fwd)) return fwd ? 2 : (L.max_upd > 0 ? 2 : 1);
   const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
   if (fwd) return slices;
   return 1 + (L.max_k > 0 ? slices : 0);

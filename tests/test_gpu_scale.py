@@ -90,14 +90,19 @@ print("ok", res)
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["front", "split"])
 @pytest.mark.parametrize("shape,limit", [((512, 512), 112), ((256, 256), 1), ((16, 16, 16), 1)])
-def test_forced_front_sweeps(shape, limit, cuda_ok):
-    """The CTA-per-front forward and backward sweeps on every large level with
-    k > 64 (thresholds lowered through the environment, fresh process)."""
+def test_forced_front_sweeps(shape, limit, mode, cuda_ok):
+    """The CTA-per-front (or split: pivot rows per front + update-row chunks)
+    forward and backward sweeps on every large level with k > 64 (thresholds
+    lowered through the environment, fresh process)."""
     import os, subprocess, sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
-    env = dict(os.environ, TFB_FRONT_SOLVE="2", TFB_FRONT_MIN_FRONTS="1")
+    if mode == "front":
+        env = dict(os.environ, TFB_FRONT_SOLVE="2", TFB_FRONT_MIN_FRONTS="1")
+    else:
+        env = dict(os.environ, TFB_FRONT_SOLVE="0", TFB_SPLIT_SOLVE="2")
     out = subprocess.run([sys.executable, "-c", _FORCED_SWEEPS.format(root=root, shape=shape, limit=limit)],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
