@@ -290,7 +290,18 @@ __global__ void __launch_bounds__(G* GPC)
 constexpr int TB = 64;         // tile rows = pivot block width (= factorization NB)
 constexpr int TLD = TB + 4;    // shared tile row stride (conflict-free 4-thread dots)
 constexpr int kWaveCols = 32;  // RHS columns per launch
-constexpr int kWaveFewFronts = 64;  // at most this many fronts: prefetch-heavy tile buffers
+// At most this many fronts: prefetch-heavy tile buffers (fewer CTAs per SM).
+// Measured on cfg5: the forward sweep wants them only up to 8 fronts (from
+// 16 fronts up one buffer and more resident CTAs win, 15-25%), the backward
+// one up to 64.  TFB_WAVE_FEW overrides both (tuning sweeps).
+static int wave_few_fronts(bool fwd) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TFB_WAVE_FEW");
+    v = e ? atoi(e) : -1;
+  }
+  return v >= 0 ? v : (fwd ? 8 : 64);
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -1613,7 +1624,7 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
   int* flags = reinterpret_cast<int*>(work + wave_blocks_doubles(L, nrhs));
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
-    const int nbuf = L.n_fronts <= kWaveFewFronts ? 3 : 1;
+    const int nbuf = L.n_fronts <= wave_few_fronts(true) ? 3 : 1;
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
     if (nb > 0) cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb, st);
     timer_begin(K_SOLVE_FWD_WAVE, st);
@@ -1696,7 +1707,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   for (int b = 0; b < nb; b++) ntiles += (long long)L.n_fronts * (std::max(0, rt - b - 2) + 1);
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
-    const int nbuf = L.n_fronts <= kWaveFewFronts ? 2 : 1;
+    const int nbuf = L.n_fronts <= wave_few_fronts(false) ? 2 : 1;
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr + 4 * TB);
     cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb * (1 + rt), st);
     timer_begin(K_SOLVE_BWD_WAVE, st);
