@@ -1384,7 +1384,7 @@ static bool split_solve(const LevelArgs& L, int nrhs, bool fwd) {
     v = e ? atoi(e) : 1;
   }
   if (v == 0 || (fwd && v < 2)) return false;
-  return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= (v >= 2 ? 1 : 32) &&
+  return nrhs == 1 && L.max_k > 0 && L.level_fronts >= (v >= 2 ? 1 : 32) &&
          (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
 
@@ -1401,7 +1401,7 @@ static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
   }
   if (v == 0) return false;
   const long long need = min_fronts > 0 ? min_fronts : 256;
-  return nrhs == 1 && L.max_k > 2 * 32 && L.level_fronts >= need &&
+  return nrhs == 1 && L.max_k > 0 && L.level_fronts >= need &&
          (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
 
@@ -1411,7 +1411,9 @@ static bool narrow_solve(const LevelArgs& L, int nrhs) {
     const char* e = getenv("TFB_NARROW_SOLVE");
     v = e ? atoi(e) != 0 : 1;
   }
-  return v && nrhs == 1 && L.max_k > 0 && L.max_k <= 2 * 32 &&
+  // a warp per front needs many fronts to fill the GPU (cfg5: >= 2048);
+  // fewer fronts take the CTA-per-front / split / wavefront sweeps
+  return v && nrhs == 1 && L.max_k > 0 && L.max_k <= 2 * 32 && L.level_fronts >= 1024 &&
          (size_t)kNarrowWarps * L.max_m * 8 <= 200 * 1024;
 }
 
