@@ -1317,7 +1317,7 @@ __global__ void __launch_bounds__(256)
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
   const int rs = k + blockIdx.y * kSplitRows, c0 = blockIdx.z * TB;
-  if (rs >= m || c0 >= k) return;
+  if (rs >= m || (c0 >= k && blockIdx.z > 0)) return;  // block 0 always serves X (k may be 0)
   const int re = min(m, rs + kSplitRows), kb = min(TB, k - c0);
   const double* Pf = factors + f * L.fac_stride;
   if (has_parent) {
@@ -1334,6 +1334,7 @@ __global__ void __launch_bounds__(256)
     double* Xo = x_out + f * out_rows * ldr + col0;
     for (int r = rs + tid; r < re; r += 256) Xo[(long long)r * ldr] = Xs[r - rs];
   }
+  if (kb <= 0) return;  // a front without pivots: X rows only
   double acc[2] = {0.0, 0.0};
   const double* Pc = Pf + c0;
   int r = rs + warp;

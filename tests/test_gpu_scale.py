@@ -91,7 +91,8 @@ print("ok", res)
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["front", "split"])
-@pytest.mark.parametrize("shape,limit", [((512, 512), 112), ((256, 256), 1), ((16, 16, 16), 1)])
+@pytest.mark.parametrize("shape,limit", [((512, 512), 112), ((256, 256), 1), ((16, 16, 16), 1),
+                                         ((1000,), 1)])
 def test_forced_front_sweeps(shape, limit, mode, cuda_ok):
     """The CTA-per-front (or split: pivot rows per front + update-row chunks)
     forward and backward sweeps on every large level with k > 64 (thresholds
