@@ -1168,7 +1168,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // Measured on cfg5 (k = 128, 256): the CTA-per-front sweeps beat the
-// wavefront kernels from 256 fronts up (backward 1.2-2.5x, forward 5-15%);
+// wavefront kernels from 256 fronts up backward (1.2-2.5x) and from 512 up
+// forward (5-15%);
 // below that the wavefront's tile parallelism wins
 // (TFB_FRONT_SOLVE=0 disables both; TFB_FRONT_MIN_FRONTS overrides the bound).
 // ----------------------------------------- small fronts, one RHS, 8 < k <= 16
@@ -1401,7 +1402,7 @@ static bool front_solve(const LevelArgs& L, int nrhs, bool fwd) {
     min_fronts = e ? atoll(e) : 0;
   }
   if (v == 0) return false;
-  const long long need = min_fronts > 0 ? min_fronts : 256;
+  const long long need = min_fronts > 0 ? min_fronts : (fwd ? 512 : 256);
   return nrhs == 1 && L.max_k > 0 && L.level_fronts >= need &&
          (size_t)(L.max_m + 9 * TB) * 8 <= 200 * 1024;
 }
