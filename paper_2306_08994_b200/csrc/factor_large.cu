@@ -457,7 +457,11 @@ __global__ void __launch_bounds__(256) large_diag64_kernel(LevelArgs L, double* 
 // tile as a DMMA product P_rb <- (P_rb M^T) D^-1.  The CTA of row tile 0 also
 // writes d and the aux block.
 constexpr int TRB = 64;
-constexpr int kFusedBlockMaxFronts = 2;
+// Measured (cfg5 L23, 64^3 L17): at 2 fronts the redundant per-CTA diagonal
+// factorizations steal more SM time from the concurrent Schur stream than the
+// separate TRSM launch costs (5.29 -> 4.67 ms); the fused kernel now serves
+// single-front levels only (the root when TFB_ROOT_DATAFLOW=0)
+constexpr int kFusedBlockMaxFronts = 1;
 constexpr int ALD = NB + 4;
 constexpr size_t kBlockSmem = sizeof(double) * (2 * NB * DLD + TRB * ALD + NB);
 
