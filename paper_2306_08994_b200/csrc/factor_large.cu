@@ -901,7 +901,7 @@ static int lookahead_root_cols() {
   return v;
 }
 static int lookahead_width(int max_upd) { return max_upd > 0 ? lookahead_cols() : lookahead_root_cols(); }
-constexpr int kLookaheadMaxFronts = 64;  // measured: 32-64 fronts gain ~1% since the chain kernels got faster
+constexpr int kLookaheadMaxFronts = 64;  // measured: 32-64 fronts gain ~1% (cfg5 L18-L19)
 
 struct LookaheadStreams {
   cudaStream_t chain = nullptr, panel = nullptr, schur = nullptr;
