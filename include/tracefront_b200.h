@@ -111,6 +111,27 @@ int tf_plan_node_lists(const tf_plan* plan, int32_t level, int64_t* ptr, int32_t
 /* Total length of the node lists of one level. */
 int64_t tf_plan_node_lists_len(const tf_plan* plan, int32_t level);
 
+/* Statistics of the canonical atomic Foata normal form. */
+typedef struct {
+  int64_t n_tasks;   /* |alphabet| = cells + sum_steps (a + 2a^2)   (tasks.py:162-182) */
+  int64_t n_edges;   /* J1-J4 edges, counted like DependencyGraph.n_edges (tasks.py:207-252) */
+  int64_t n_cells;   /* stored positions incl. fill = number of Assertions */
+  int64_t max_width; /* widest Foata class */
+  int32_t n_classes;
+  int32_t singular;  /* pivot with no diagonal entry when TF_ERR_STRAY is returned */
+  int64_t n_divisions;       /* sum_steps a   (Subtractions: same count as Multiplications) */
+  int64_t n_multiplications; /* sum_steps a^2 */
+} tf_fnf_stats;
+
+/* Replaces build_task_graph + compute_fnf (tasks.py:360, schedule.py:60-82) for
+ * schedule statistics: streams the Diekert graph in elimination order without
+ * materialising it.  widths[c] = tasks in class c+1, kinds[c] = bitmask of
+ * TaskKinds (bit kind-1: 1 division, 2 multiplication, 3 subtraction,
+ * 4 assertion).  Pass widths = kinds = NULL to size the arrays from
+ * st->n_classes; cap is their capacity.  Needs a plan built with keep_lists. */
+int tf_atomic_fnf(const tf_plan* plan, tf_fnf_stats* st, int64_t* widths, int32_t* kinds,
+                  int32_t cap);
+
 /* ---------------------------------------------------------------- device */
 
 /* Device view of one level: the tf_level_host arrays copied to the GPU. */

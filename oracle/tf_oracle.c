@@ -10,7 +10,7 @@
  *   solve (engine.py:468-493)
  * Compiled with -ffp-contract=off so no FMA changes the rounding: its factors
  * and solutions are bitwise equal to the reference's (pinned by
- * tests/test_oracle.py against tests/golden/*.npz).  Used only by tests/,
+ * tests/test_oracle.py against the tests/golden npz files).  Used only by tests/,
  * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg.
  * Single-threaded: the per-cell subtraction chains (tasks.py:242-249) fix the
  * order of updates to shared cells, so a faithful port is sequential.

@@ -29,7 +29,8 @@ from .fem import (
 )
 from .tree import EliminationTree, TreeNode, build_elimination_tree, join_fronts, sort_fronts
 from .symbolic import EliminationPlan, NodeReorder, PivotStep, symbolic_eliminate
-from .schedule import FoataSchedule, TaskKind, compute_fnf, schedule_stats
+from .schedule import (AtomicFoataSchedule, FoataSchedule, TaskKind, compute_atomic_fnf,
+                       compute_fnf, schedule_stats, schedule_stats_csv)
 from .engine import (
     ExecState,
     FactorResult,

@@ -17,6 +17,7 @@ TF_OK = 0
 TF_ZERO_PIVOT = 2
 TF_ERR_INVALID = -1
 TF_ERR_CUDA = -2
+TF_ERR_STRAY = -3
 
 PAT_WIDTH = 12
 (PAT_M, PAT_K, PAT_NSRC, PAT_LEN0, PAT_LEN1, PAT_OFF0, PAT_OFF1, PAT_LEAF, PAT_IOFF, PAT_KP,
@@ -28,6 +29,14 @@ class PlanSummary(C.Structure):
         ("n_dof", C.c_int64), ("n_leaves", C.c_int64), ("n_nodes", C.c_int64),
         ("n_pivots", C.c_int64), ("n_levels", C.c_int32), ("max_m", C.c_int32),
         ("max_k", C.c_int32), ("keep_lists", C.c_int32),
+    ]
+
+
+class FnfStats(C.Structure):
+    _fields_ = [
+        ("n_tasks", C.c_int64), ("n_edges", C.c_int64), ("n_cells", C.c_int64),
+        ("max_width", C.c_int64), ("n_classes", C.c_int32), ("singular", C.c_int32),
+        ("n_divisions", C.c_int64), ("n_multiplications", C.c_int64),
     ]
 
 
@@ -65,7 +74,7 @@ EXPORTS = (
     "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
     "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_subtree_fusable",
     "tf_subtree_factor", "tf_timing_enable", "tf_timing_collect", "tf_timing_class_name",
-    "tf_build_info",
+    "tf_build_info", "tf_atomic_fnf",
 )
 
 _lib = None
@@ -100,6 +109,8 @@ def load() -> C.CDLL:
     lib.tf_plan_node_lists.restype = C.c_int
     lib.tf_plan_node_lists_len.argtypes = [vp, i32]
     lib.tf_plan_node_lists_len.restype = i64
+    lib.tf_atomic_fnf.argtypes = [vp, C.POINTER(FnfStats), P_i64, P_i32, i32]
+    lib.tf_atomic_fnf.restype = C.c_int
     lib.tf_level_factor_workspace.argtypes = [C.POINTER(LevelView)]
     lib.tf_level_factor_workspace.restype = i64
     lib.tf_level_aux_doubles.argtypes = [C.POINTER(LevelView)]

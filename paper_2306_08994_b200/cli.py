@@ -118,13 +118,21 @@ def cmd_generate(args, parser) -> int:
 def cmd_plan(args, parser) -> int:
     mesh = _mesh(args, parser)
     tf, system, tree, plan = _pipeline(mesh, args.rhs)
-    sched = tf.compute_fnf(plan)
-    st = tf.schedule_stats(sched)
     ls = plan.level_stats()
     print(f"n_dof={mesh.n_dof}")
     print(f"tree_depth={tree.n_levels}")
+    if plan.native.keep_lists:
+        # the reference's atomic trace (cli.py:184-196), streamed natively
+        sched = tf.compute_atomic_fnf(plan)
+        for kind in tf.TaskKind:
+            print(f"tasks_{kind.name.lower()}={sched.kind_counts[kind]}")
+        print(f"tasks_total={sched.n_tasks}")
+    else:
+        sched = tf.compute_fnf(plan)
+    st = tf.schedule_stats(sched)
     print(f"foata_classes={st.n_classes}")
     print(f"max_class_width={st.max_width}")
+    print(f"level_classes={tree.n_levels}")
     print(f"pivots={plan.native.n_pivots}")
     print(f"max_front={plan.native.max_m}")
     print(f"ldl_flops={sum(s['ldl_flops'] for s in ls):.6e}")

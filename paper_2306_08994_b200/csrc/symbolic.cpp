@@ -442,3 +442,170 @@ extern "C" int tf_plan_node_lists(const tf_plan* P, int32_t L, int64_t* ptr, int
   if (idx) std::memcpy(idx, lv.list_idx.data(), sizeof(int32_t) * lv.list_idx.size());
   return TF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Canonical atomic Diekert graph + Foata normal form, streamed.
+//
+// Replaces enumerate_tasks / build_dependency_edges (tasks.py:162-252) and
+// compute_fnf (schedule.py:60-82) for statistics and validation.  The graph
+// is never materialised: walking the pivot steps in elimination order, every
+// task's class follows from its predecessors' classes, which are final by
+// then.
+//   Assert(c)   = 1 + class(last Sub on c)      (1 when c is never updated)
+//   Div(z,y)    = 1 + max(Assert(z,y), Assert(z,z))                J1
+//   Mul(z,x,y)  = 1 + max(Div(z,y), Assert(x,z))                   J2
+//   Sub(z,x,y)  = 1 + max(Mul(z,x,y), previous Sub on (x,y))       J3
+// An Assert of row/column z is read only at step z, after which no step
+// touches that row or column again (z leaves every active set), so its class
+// is final when read (J4).  Per-pivot active sets come from the same boolean
+// dense-front simulation as symbolic.py's EliminationPlan._structure: a
+// front's pattern is the OR of its sources' patterns, and each pivot ORs its
+// fill clique (tasks.py:142-150) into the trailing block.
+namespace {
+
+struct CellTable {  // open addressing (x,y) -> class of the last Sub (0: none)
+  std::vector<uint64_t> keys;
+  std::vector<int32_t> vals;
+  uint64_t mask = 0;
+  int64_t used = 0;
+  explicit CellTable(int64_t hint) {
+    uint64_t cap = 1024;
+    while (cap < (uint64_t)(hint * 2)) cap <<= 1;
+    keys.assign(cap, ~0ULL);
+    vals.assign(cap, 0);
+    mask = cap - 1;
+  }
+  void grow() {
+    std::vector<uint64_t> ok;
+    std::vector<int32_t> ov;
+    ok.swap(keys);
+    ov.swap(vals);
+    keys.assign(ok.size() * 2, ~0ULL);
+    vals.assign(ok.size() * 2, 0);
+    mask = keys.size() - 1;
+    used = 0;
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (ok[i] != ~0ULL) slot(ok[i]) = ov[i];
+  }
+  int32_t& slot(uint64_t key) {
+    uint64_t h = mix(0, key) & mask;
+    while (keys[h] != key) {
+      if (keys[h] == ~0ULL) {
+        if ((uint64_t)(used + 1) * 10 > keys.size() * 7) {
+          grow();
+          return slot(key);
+        }
+        keys[h] = key;
+        ++used;
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+    return vals[h];
+  }
+  int32_t& at(int32_t x, int32_t y) { return slot(((uint64_t)(uint32_t)x << 32) | (uint32_t)y); }
+};
+
+}  // namespace
+
+extern "C" int tf_atomic_fnf(const tf_plan* P, tf_fnf_stats* st, int64_t* widths, int32_t* kinds,
+                             int32_t cap) {
+  if (!P || !st) return TF_ERR_INVALID;
+  if (!P->keep) return TF_ERR_INVALID;  // needs the per-node index lists
+  std::memset(st, 0, sizeof(*st));
+  std::vector<int64_t> w;
+  std::vector<int32_t> kd;
+  auto bump = [&](int32_t c, int kind, int64_t cnt) {
+    if ((size_t)c > w.size()) {
+      w.resize(c, 0);
+      kd.resize(c, 0);
+    }
+    w[c - 1] += cnt;
+    kd[c - 1] |= 1 << (kind - 1);
+  };
+  int64_t n_edges = 0, n_steps_tasks = 0;
+  CellTable cells(P->n_dof * 16);
+  std::vector<std::vector<uint8_t>> prev, cur;
+  std::vector<std::pair<int32_t, int32_t>> act;  // (global, position)
+  std::vector<int32_t> divc;
+  for (int32_t L = 0; L < P->n_levels; ++L) {
+    const Level& lv = P->levels[L];
+    cur.assign(lv.n_fronts, {});
+    for (int32_t i = 0; i < lv.n_fronts; ++i) {
+      const int32_t* row = &lv.pat[(size_t)lv.pattern_of[i] * TF_PAT_WIDTH];
+      const int32_t m = row[TF_PAT_M], k = row[TF_PAT_K], nsrc = row[TF_PAT_NSRC];
+      std::vector<uint8_t> B((size_t)m * m, 0);
+      for (int32_t c = 0; c < nsrc; ++c) {
+        const int32_t* mp = &lv.maps[row[TF_PAT_OFF0 + c]];
+        const int32_t len = row[TF_PAT_LEN0 + c];
+        const uint8_t* src = L == 0 ? nullptr : prev[2 * (size_t)i + c].data();
+        for (int32_t a = 0; a < len; ++a)
+          for (int32_t b = 0; b < len; ++b)
+            if (!src || src[(size_t)a * len + b]) B[(size_t)mp[a] * m + mp[b]] = 1;
+      }
+      const int32_t* lst = &lv.list_idx[lv.list_ptr[i]];
+      for (int32_t c = 0; c < k; ++c) {
+        const int32_t z = lst[c];
+        if (!B[(size_t)c * m + c]) {
+          st->singular = z;
+          return TF_ERR_STRAY;
+        }
+        act.clear();
+        for (int32_t j = c + 1; j < m; ++j)
+          if (B[(size_t)c * m + j]) act.emplace_back(lst[j], j);
+        std::sort(act.begin(), act.end());
+        const int64_t a = (int64_t)act.size();
+        n_steps_tasks += a + 2 * a * a;
+        st->n_divisions += a;
+        st->n_multiplications += a * a;
+        const int32_t azz = 1 + cells.at(z, z);
+        divc.resize(a);
+        for (int64_t q = 0; q < a; ++q) {
+          divc[q] = 1 + std::max(1 + cells.at(z, act[q].first), azz);
+          bump(divc[q], 1, 1);
+        }
+        n_edges += 2 * a + 3 * a * a;  // J1, J2 (two each), J3 Mul -> Sub
+        for (int64_t p = 0; p < a; ++p) {
+          const int32_t x = act[p].first;
+          const int32_t axz = 1 + cells.at(x, z);
+          for (int64_t q = 0; q < a; ++q) {
+            const int32_t mul = 1 + std::max(divc[q], axz);
+            bump(mul, 2, 1);
+            int32_t& s = cells.at(x, act[q].first);
+            if (s) ++n_edges;  // J3 chain
+            s = 1 + std::max(mul, s);
+            bump(s, 3, 1);
+          }
+        }
+        for (int64_t p = 0; p < a; ++p) {  // fill clique
+          const int32_t pp = act[p].second;
+          for (int64_t q = 0; q < a; ++q) B[(size_t)pp * m + act[q].second] = 1;
+        }
+      }
+      const int32_t u = m - k;
+      cur[i].resize((size_t)u * u);
+      for (int32_t r = 0; r < u; ++r)
+        std::memcpy(&cur[i][(size_t)r * u], &B[(size_t)(k + r) * m + k], u);
+    }
+    prev.swap(cur);
+  }
+  for (size_t h = 0; h < cells.keys.size(); ++h) {
+    if (cells.keys[h] == ~0ULL) continue;
+    const int32_t s = cells.vals[h];
+    if (s) ++n_edges;  // J4
+    bump(1 + s, 4, 1);
+  }
+  st->n_cells = cells.used;
+  st->n_tasks = cells.used + n_steps_tasks;
+  st->n_edges = n_edges;
+  st->n_classes = (int32_t)w.size();
+  int64_t mx = 0;
+  for (int64_t v : w) mx = std::max(mx, v);
+  st->max_width = mx;
+  if (widths && kinds) {
+    if (cap < (int32_t)w.size()) return TF_ERR_INVALID;
+    std::copy(w.begin(), w.end(), widths);
+    std::copy(kd.begin(), kd.end(), kinds);
+  }
+  return TF_OK;
+}

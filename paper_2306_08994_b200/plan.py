@@ -83,6 +83,23 @@ class NativePlan:
         _lib.check(lib.tf_plan_pivot_order(h, _lib.i32p(po)), "tf_plan_pivot_order")
         self.pivot_order = po
 
+    def atomic_fnf(self):
+        """(FnfStats, widths[int64], kinds[int32]) of the atomic Foata normal form."""
+        if not self.keep_lists:
+            raise RuntimeError("atomic FNF needs a plan built with keep_lists")
+        st = _lib.FnfStats()
+        rc = self._lib.tf_atomic_fnf(self._h, C.byref(st), None, None, 0)
+        if rc == _lib.TF_ERR_STRAY:
+            from .errors import SymbolicSingularityError
+            raise SymbolicSingularityError(int(st.singular))
+        _lib.check(rc, "tf_atomic_fnf")
+        n = max(int(st.n_classes), 1)
+        widths = np.zeros(n, dtype=np.int64)
+        kinds = np.zeros(n, dtype=np.int32)
+        _lib.check(self._lib.tf_atomic_fnf(self._h, C.byref(st), _lib.i64p(widths),
+                                           _lib.i32p(kinds), n), "tf_atomic_fnf")
+        return st, widths[:st.n_classes], kinds[:st.n_classes]
+
     def _level(self, L: int) -> LevelTables:
         lh = _lib.LevelHost()
         _lib.check(self._lib.tf_plan_level(self._h, L, C.byref(lh)), "tf_plan_level")

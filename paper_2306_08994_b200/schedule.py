@@ -71,7 +71,46 @@ def compute_fnf(plan) -> FoataSchedule:
                          level_sizes=tuple(plan.tree.level_sizes))
 
 
-def schedule_stats(schedule: FoataSchedule) -> ScheduleStats:
+@dataclass(frozen=True)
+class AtomicFoataSchedule:
+    """Canonical FNF of the reference's atomic trace (schedule.py:60-82), as statistics.
+
+    Computed natively (`tf_atomic_fnf`, csrc/symbolic.cpp) by streaming the
+    Diekert graph of tasks.py:162-252 in elimination order; per-task class
+    lists are not materialised.  `widths[c]` and `class_kinds[c]` equal
+    `len(compute_fnf(graph).classes[c])` and `class_kinds[c]` of the reference.
+    """
+
+    n_tasks: int
+    n_edges: int
+    n_cells: int
+    kind_counts: dict
+    widths: tuple[int, ...]
+    class_kinds: tuple[frozenset, ...]
+
+    @property
+    def n_classes(self) -> int:
+        return len(self.widths)
+
+    @property
+    def level_sizes(self) -> tuple[int, ...]:
+        return self.widths
+
+
+def compute_atomic_fnf(plan) -> AtomicFoataSchedule:
+    """Atomic-granularity FNF statistics of `plan` (needs a plan small enough to keep node lists)."""
+    st, widths, kinds = plan.native.atomic_fnf()
+    ks = tuple(frozenset(k for k in TaskKind if int(m) >> (int(k) - 1) & 1) for m in kinds)
+    return AtomicFoataSchedule(n_tasks=int(st.n_tasks), n_edges=int(st.n_edges),
+                               n_cells=int(st.n_cells),
+                               kind_counts={TaskKind.DIVISION: int(st.n_divisions),
+                                            TaskKind.MULTIPLICATION: int(st.n_multiplications),
+                                            TaskKind.SUBTRACTION: int(st.n_multiplications),
+                                            TaskKind.ASSERTION: int(st.n_cells)},
+                               widths=tuple(int(w) for w in widths), class_kinds=ks)
+
+
+def schedule_stats(schedule) -> ScheduleStats:
     widths = tuple(schedule.level_sizes)
     mixed = tuple(i + 1 for i, ks in enumerate(schedule.class_kinds)
                   if TaskKind.DIVISION in ks and TaskKind.SUBTRACTION in ks)
@@ -80,7 +119,7 @@ def schedule_stats(schedule: FoataSchedule) -> ScheduleStats:
                          mixed_classes=mixed)
 
 
-def schedule_stats_csv(schedule: FoataSchedule) -> str:
+def schedule_stats_csv(schedule) -> str:
     lines = ["class_index,kind_set,size"]
     for i, (w, ks) in enumerate(zip(schedule.level_sizes, schedule.class_kinds)):
         lines.append(f"{i + 1},{'|'.join(sorted(k.name.lower() for k in ks))},{w}")
