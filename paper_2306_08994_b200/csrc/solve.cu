@@ -52,6 +52,13 @@ __device__ __forceinline__ void stage_panel(double* Ls, const double* __restrict
   for (int c = t; c < k; c += G) Ls[n + c] = __ldg(P + (long long)m * kp + c);
 }
 
+// Row/column split of a flat index over nr columns: a shift when nr is a
+// power of two (the dispatcher slices columns that way), else a division.
+#define TFB_DIV_SETUP(nr_) \
+  const bool div_p2 = ((nr_) & ((nr_)-1)) == 0; \
+  const int div_lg = 31 - __clz(nr_)
+#define TFB_DIV(e_) (div_p2 ? ((e_) >> div_lg) : ((e_) / nr))
+
 // Vectors: row stride ldr (total RHS columns); this launch handles columns
 // [col0, col0 + nr).  With one column (nr == 1) every panel entry is used
 // exactly once, so the panel is read straight from global memory and shared
@@ -78,6 +85,7 @@ __global__ void __launch_bounds__(G* GPC)
                     int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
+  TFB_DIV_SETUP(nr);
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
   if (f >= L.n_fronts) return;
@@ -97,7 +105,7 @@ __global__ void __launch_bounds__(G* GPC)
   }
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nW; e += G) {
-    const int r = e / nr, j = e - r * nr;
+    const int r = TFB_DIV(e), j = e - r * nr;
     W[e] = e < nK ? y[(piv + r) * ldr + col0 + j] : 0.0;
   }
   group_sync<G>(bar);
@@ -116,7 +124,7 @@ __global__ void __launch_bounds__(G* GPC)
         double v[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          const int eq = e + q * G, a = eq / nr, j = eq - a * nr;
+          const int eq = e + q * G, a = TFB_DIV(eq), j = eq - a * nr;
           p[q] = __ldg(mp + a) * nr + j;
           v[q] = Wc[(long long)a * ldr + j];
         }
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(G* GPC)
         for (int q = 0; q < 4; q++) W[p[q]] += v[q];
       }
       for (; e < n; e += G) {
-        const int a = e / nr, j = e - a * nr;
+        const int a = TFB_DIV(e), j = e - a * nr;
         W[mp[a] * nr + j] += Wc[(long long)a * ldr + j];
       }
       group_sync<G>(bar);
@@ -135,13 +143,13 @@ __global__ void __launch_bounds__(G* GPC)
     const int n = (k - c - 1) * nr;
     const double* Wc = W + c * nr;
     for (int e = t; e < n; e += G) {
-      const int r = c + 1 + e / nr, j = e % nr;
+      const int q = TFB_DIV(e), r = c + 1 + q, j = e - q * nr;
       W[r * nr + j] -= Lp(r, c) * Wc[j];
     }
     group_sync<G>(bar);
   }
   for (int e = t; e < nK; e += G) {
-    const int r = e / nr, j = e - r * nr;
+    const int r = TFB_DIV(e), j = e - r * nr;
     y[(piv + r) * ldr + col0 + j] = W[e] / dv[r];
   }
   // update rows: w_r - l_r . w_piv (row-contiguous panel reads), straight out
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(G* GPC)
     return;
   }
   for (int e = nK + t; e < nW; e += G) {
-    const int r = e / nr, j = e - r * nr;
+    const int r = TFB_DIV(e), j = e - r * nr;
     double acc = W[e];
     for (int c = 0; c < k; c++) acc -= Lp(r, c) * W[c * nr + j];
     out[(long long)(r - k) * ldr + j] = acc;
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(G* GPC)
                     int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
+  TFB_DIV_SETUP(nr);
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
   const long long f = (long long)blockIdx.x * GPC + gid;
   if (f >= L.n_fronts) return;
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(G* GPC)
   }
   const int nW = m * nr, nK = k * nr;
   for (int e = t; e < nK; e += G) {
-    const int r = e / nr, j = e - r * nr;
+    const int r = TFB_DIV(e), j = e - r * nr;
     X[e] = y[(piv + r) * ldr + col0 + j];
   }
   if (has_parent && m > k) {
@@ -210,14 +219,14 @@ __global__ void __launch_bounds__(G* GPC)
       double v[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int eq = e + q * G - nK, a = eq / nr, j = eq - a * nr;
+        const int eq = e + q * G - nK, a = TFB_DIV(eq), j = eq - a * nr;
         v[q] = Xp[(long long)__ldg(mp + a) * ldr + j];
       }
 #pragma unroll
       for (int q = 0; q < 4; q++) X[e + q * G] = v[q];
     }
     for (; e < nW; e += G) {
-      const int a = (e - nK) / nr, j = (e - nK) % nr;
+      const int a = TFB_DIV(e - nK), j = (e - nK) - a * nr;
       X[e] = Xp[(long long)mp[a] * ldr + j];
     }
   }
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(G* GPC)
     group_sync<G>(bar);
   } else if (m > k) {
     for (int e = t; e < nK; e += G) {
-      const int c = e / nr, j = e - c * nr;
+      const int c = TFB_DIV(e), j = e - c * nr;
       double acc = X[e];
       for (int r = k; r < m; r++) acc -= Lp(r, c) * X[r * nr + j];
       X[e] = acc;
@@ -254,19 +263,19 @@ __global__ void __launch_bounds__(G* GPC)
     const double* Xc = X + c * nr;
     const int n = c * nr;
     for (int e = t; e < n; e += G) {
-      const int r = e / nr, j = e - r * nr;
+      const int r = TFB_DIV(e), j = e - r * nr;
       X[e] -= Lp(c, r) * Xc[j];
     }
     group_sync<G>(bar);
   }
   for (int e = t; e < nK; e += G) {
-    const int r = e / nr, j = e - r * nr;
+    const int r = TFB_DIV(e), j = e - r * nr;
     y[(piv + r) * ldr + col0 + j] = X[e];
   }
   if (!L.is_leaf) {
     double* out = x_out + f * out_rows * ldr + col0;
     for (int e = t; e < nW; e += G) {
-      const int r = e / nr, j = e - r * nr;
+      const int r = TFB_DIV(e), j = e - r * nr;
       out[(long long)r * ldr + j] = X[e];
     }
   }
@@ -382,6 +391,7 @@ __global__ void __launch_bounds__(256)
   double* Wt = T0 + nbuf * TB * TLD;  // [TB][nr]
   double* Yb = Wt + TB * nr;          // [TB][nr]
   const int tid = threadIdx.x;
+  TFB_DIV_SETUP(nr);
   const long long nf = L.n_fronts, ntiles = (long long)rt_max * nf;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int R = (int)(tile / nf);
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(256)
       }
       const int* inv = L.maps + s.ioff;
       for (int e = tid; e < TB * nr; e += 256) {
-        const int rl = ONE ? e : e / nr, j = ONE ? 0 : e - rl * nr, r = r0 + rl;
+        const int rl = ONE ? e : TFB_DIV(e), j = ONE ? 0 : e - rl * nr, r = r0 + rl;
         double v = 0.0;
         if (rl < rows) {
           if (r < k) v = y[(piv + r) * ldr + col0 + j];
@@ -443,7 +453,7 @@ __global__ void __launch_bounds__(256)
         if ((tid & 3) == 0 && (tid >> 2) < rows) Wt[tid >> 2] -= sdot;
       } else {
         for (int e = tid; e < rows * nr; e += 256) {
-          const int i = e / nr, j = e - i * nr;
+          const int i = TFB_DIV(e), j = e - i * nr;
           Wt[e] -= tile_dot_col<false, 0>(T, Yb, i, j, nr, kb);
         }
       }
@@ -463,14 +473,14 @@ __global__ void __launch_bounds__(256)
         if ((tid & 3) == 0) Yb[i] = i < kb ? Wt[i] + sdot : 0.0;
       } else {
         for (int e = tid; e < TB * nr; e += 256) {
-          const int i = e / nr, j = e - i * nr;
+          const int i = TFB_DIV(e), j = e - i * nr;
           Yb[e] = i < kb ? Wt[e] + tile_dot_col<false, -1>(Mt, Wt, i, j, nr, kb) : 0.0;
         }
       }
       __syncthreads();
       const double* dv = Pf + (long long)m * kp + r0;
       for (int e = tid; e < kb * nr; e += 256) {
-        const int c = ONE ? e : e / nr, j = ONE ? 0 : e - c * nr;
+        const int c = ONE ? e : TFB_DIV(e), j = ONE ? 0 : e - c * nr;
         yb[(long long)R * TB * nr + e] = Yb[e];
         y[(piv + r0 + c) * ldr + col0 + j] = Yb[e] / dv[c];
       }
@@ -1459,7 +1469,10 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
 static int small_cols(const LevelArgs& L, int nrhs) {
   const long long fixed = (long long)L.max_m * L.max_k + L.max_m;
   const int cmax = (int)((kSmallSolveSmem / 8 - fixed) / std::max(L.max_m, 1));
-  return std::max(1, std::min(nrhs, cmax));
+  if (nrhs <= cmax) return std::max(1, nrhs);
+  int cw = 1;  // sliced anyway: power-of-two slices keep the kernels' index split a shift
+  while (cw * 2 <= cmax) cw *= 2;
+  return cw;
 }
 
 // flag: forward -- 1 if the child level's update rows start at row 0 of its
