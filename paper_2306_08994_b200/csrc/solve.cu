@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(G* GPC)
   double* W = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  if (L.is_leaf && k == 0) return;  // element without pivots: its update block is 0 (memset)
+  if (L.is_leaf && k == 0) return;  // element without pivots: zero update, not written (parent skips it)
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(G* GPC)
   if (!L.is_leaf) {
     for (int c = 0; c < s.nsrc; c++) {
       const long long ch = 2 * (L.front_base + f) + c - C.front_base;
-      const int off =
-          child_at0 ? 0 : C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
+      const int ck = C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
+      if (C.is_leaf && ck == 0) continue;  // element without pivots: zero update, never written
+      const int off = child_at0 ? 0 : ck;
       const int len = c == 0 ? s.len0 : s.len1;
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
       const double* Wc = w_child + (ch * child_rows + off) * ldr + col0;
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(G* GPC)
 //             z = y_b - (L[b+1, b]^T X_{b+1} + sum_R P_R), X_b = M_b^T z.
 constexpr int TB = 64;         // tile rows = pivot block width (= factorization NB)
 constexpr int TLD = TB + 4;    // shared tile row stride (conflict-free 4-thread dots)
-constexpr int kWaveCols = 32;  // RHS columns per launch
+constexpr int kWaveCols = 64;  // RHS columns per launch (tile_prod covers up to 64)
 // At most this many fronts: prefetch-heavy tile buffers (fewer CTAs per SM).
 // Measured on cfg5: the forward sweep wants them only up to 8 fronts (from
 // 16 fronts up one buffer and more resident CTAs win, 15-25%), the backward
@@ -362,6 +363,46 @@ __device__ __forceinline__ double tile_dot(const double* T, const double* v, int
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   s += __shfl_xor_sync(0xffffffffu, s, 2);
   return s;
+}
+// Several columns: s(i, j) = sum_{c < nc} T[i][c] v[c*nr + j] (TRANS: T[c][i]),
+// masked like tile_dot, for i < ni and j < nr <= 64; f(i, j, s) is called once
+// per output.  Register-blocked: thread (tid >> 4, tid & 15) owns rows
+// ig + 16p and columns jg + 16q (p, q < 4), so each shared load feeds four
+// FMAs instead of one.  c runs in order: sums are deterministic.
+template <bool TRANS, int MASK, class F>
+__device__ __forceinline__ void tile_prod(const double* T, const double* v, int nr, int ni, int nc,
+                                          F f) {
+  const int ig = threadIdx.x >> 4, jg = threadIdx.x & 15;
+  double s[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; p++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) s[p][q] = 0.0;
+  for (int c = 0; c < nc; c++) {
+    double tv[4], vv[4];
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      const int i = ig + 16 * p;
+      const bool on = MASK == 0 || (MASK < 0 ? c < i : c > i);
+      tv[p] = on ? (TRANS ? T[c * TLD + i] : T[i * TLD + c]) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int j = jg + 16 * q;
+      vv[q] = j < nr ? v[c * nr + j] : 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) s[p][q] = fma(tv[p], vv[q], s[p][q]);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; p++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int i = ig + 16 * p, j = jg + 16 * q;
+      if (i < ni && j < nr) f(i, j, s[p][q]);
+    }
 }
 // General column count: entry (i, j) of the same product, v row stride nr.
 template <bool TRANS, int MASK>
@@ -452,10 +493,8 @@ __global__ void __launch_bounds__(256)
         const double sdot = tile_dot<false, 0>(T, Yb, kb);
         if ((tid & 3) == 0 && (tid >> 2) < rows) Wt[tid >> 2] -= sdot;
       } else {
-        for (int e = tid; e < rows * nr; e += 256) {
-          const int i = TFB_DIV(e), j = e - i * nr;
-          Wt[e] -= tile_dot_col<false, 0>(T, Yb, i, j, nr, kb);
-        }
+        tile_prod<false, 0>(T, Yb, nr, rows, kb,
+                            [&](int i, int j, double v) { Wt[i * nr + j] -= v; });
       }
       __syncthreads();
       if (nbuf == 1 && b + 1 < bend)
@@ -472,10 +511,9 @@ __global__ void __launch_bounds__(256)
         const int i = tid >> 2;
         if ((tid & 3) == 0) Yb[i] = i < kb ? Wt[i] + sdot : 0.0;
       } else {
-        for (int e = tid; e < TB * nr; e += 256) {
-          const int i = TFB_DIV(e), j = e - i * nr;
-          Yb[e] = i < kb ? Wt[e] + tile_dot_col<false, -1>(Mt, Wt, i, j, nr, kb) : 0.0;
-        }
+        tile_prod<false, -1>(Mt, Wt, nr, TB, kb, [&](int i, int j, double v) {
+          Yb[i * nr + j] = i < kb ? Wt[i * nr + j] + v : 0.0;
+        });
       }
       __syncthreads();
       const double* dv = Pf + (long long)m * kp + r0;
@@ -494,10 +532,9 @@ __global__ void __launch_bounds__(256)
           const int i = tid >> 2;
           if ((tid & 3) == 0 && i >= kb && i < rows) Wt[i] -= sdot;
         } else {
-          for (int e = tid; e < rows * nr; e += 256) {
-            const int i = e / nr, j = e - i * nr;
-            if (i >= kb) Wt[e] -= tile_dot_col<false, 0>(T0, Yb, i, j, nr, kb);
-          }
+          tile_prod<false, 0>(T0, Yb, nr, rows, kb, [&](int i, int j, double v) {
+            if (i >= kb) Wt[i * nr + j] -= v;
+          });
         }
         __syncthreads();
       }
@@ -593,10 +630,8 @@ __global__ void __launch_bounds__(256)
           const double sdot = tile_dot<true, 0>(T, Xs, rows);
           if ((tid & 3) == 0) pp[tid >> 2] = sdot;
         } else {
-          for (int e = tid; e < kb * nr; e += 256) {
-            const int c = e / nr, j = e - c * nr;
-            pp[e] = tile_dot_col<true, 0>(T, Xs, c, j, nr, rows);
-          }
+          tile_prod<true, 0>(T, Xs, nr, kb, rows,
+                             [&](int c, int j, double v) { pp[c * nr + j] = v; });
         }
         wave_publish(flp + (f * rt_max + R) * (long long)nb_max + b);
         __syncthreads();
@@ -621,10 +656,8 @@ __global__ void __launch_bounds__(256)
           const double sdot = tile_dot<true, 0>(T, Xs, rows);
           if ((tid & 3) == 0) Z[tid >> 2] = sdot;
         } else {
-          for (int e = tid; e < kb * nr; e += 256) {
-            const int c = e / nr, j = e - c * nr;
-            Z[e] = tile_dot_col<true, 0>(T, Xs, c, j, nr, rows);
-          }
+          tile_prod<true, 0>(T, Xs, nr, kb, rows,
+                             [&](int c, int j, double v) { Z[c * nr + j] = v; });
         }
         __syncthreads();
       }
@@ -661,10 +694,8 @@ __global__ void __launch_bounds__(256)
           const double sdot = tile_dot<true, 0>(T, Xs, rows1);
           if ((tid & 3) == 0) Z[tid >> 2] += sdot;
         } else {
-          for (int e = tid; e < kb * nr; e += 256) {
-            const int c = e / nr, j = e - c * nr;
-            Z[e] += tile_dot_col<true, 0>(T, Xs, c, j, nr, rows1);
-          }
+          tile_prod<true, 0>(T, Xs, nr, kb, rows1,
+                             [&](int c, int j, double v) { Z[c * nr + j] += v; });
         }
       }
       __syncthreads();
@@ -685,12 +716,11 @@ __global__ void __launch_bounds__(256)
           y[(piv + j0 + c) * ldr + col0] = xv;
         }
       } else {
-        for (int e = tid; e < kb * nr; e += 256) {
-          const int c = e / nr, j = e - c * nr;
-          const double xv = Z[e] + tile_dot_col<true, 1>(Mt, Z, c, j, nr, kb);
+        tile_prod<true, 1>(Mt, Z, nr, kb, kb, [&](int c, int j, double v) {
+          const double xv = Z[c * nr + j] + v;
           Xf[(long long)(j0 + c) * ldr + j] = xv;
           y[(piv + j0 + c) * ldr + col0 + j] = xv;
-        }
+        });
       }
       wave_publish(flx + f * nb_max + b);
       __syncthreads();
@@ -1498,10 +1528,6 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
     return cudaGetLastError();
   }
   const int cw = small_cols(L, nrhs);
-  if (FWD && L.is_leaf) {  // fronts without pivots leave zero update blocks
-    cudaError_t e = cudaMemsetAsync(w_out, 0, sizeof(double) * (size_t)L.n_fronts * out_rows * nrhs, st);
-    if (e != cudaSuccess) return e;
-  }
   for (int col0 = 0; col0 < nrhs; col0 += cw) {
     const int nr = std::min(cw, nrhs - col0);
     const long long work = (long long)L.max_m * nr;
@@ -1585,12 +1611,31 @@ static unsigned wave_grid(K kern, size_t smem, long long ntiles) {
   return (unsigned)std::max(1LL, std::min(ntiles, cap));
 }
 
+// Zero the update blocks of leaf elements without pivots (the leaf sweep
+// skips them) for parent kernels that read every child block.
+__global__ void __launch_bounds__(256)
+    zero_unpivoted_leaf_blocks(LevelArgs C, double* w, long long per_front) {
+  for (long long f = blockIdx.x; f < C.n_fronts; f += gridDim.x) {
+    if (C.pat[(size_t)C.pattern_of[f] * TF_PAT_WIDTH + TF_PAT_K] != 0) continue;
+    for (long long i = threadIdx.x; i < per_front; i += blockDim.x) w[f * per_front + i] = 0.0;
+  }
+}
+
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
                              long long out_rows, double* y, int nrhs, double* work,
                              long long work_doubles, cudaStream_t st) {
   const int child_at0 = level_is_large(C.is_leaf, C.max_m) ? 0 : 1;
-  if (!level_is_large(L.is_leaf, L.max_m))
+  // Leaf elements without pivots never write their (zero) update blocks; the
+  // group kernels skip such children, every other kernel gets them zeroed.
+  const bool small = !level_is_large(L.is_leaf, L.max_m);
+  if (C.is_leaf && w_child && C.n_fronts > 0 && (!small || warp16_solve(L, nrhs))) {
+    zero_unpivoted_leaf_blocks<<<(unsigned)std::min<long long>(C.n_fronts, 148 * 8), 256, 0, st>>>(
+        C, const_cast<double*>(w_child), child_rows * nrhs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (small)
     return dispatch_small<true>(L, C, child_at0, factors, w_child, child_rows, w_out, out_rows, y,
                                 nrhs, st);
   if (narrow_solve(L, nrhs)) {
