@@ -487,7 +487,17 @@ __global__ void __launch_bounds__(256)
       }
       wave_wait(fl + b);
       const int kb = min(TB, k - b * TB);
-      for (int e = tid; e < TB * nr; e += 256) Yb[e] = e < kb * nr ? __ldcg(yb + (long long)b * TB * nr + e) : 0.0;
+      for (int e0 = tid; e0 < TB * nr; e0 += 8 * 256) {  // eight loads in flight
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const int e = e0 + q * 256;
+          v[q] = e < kb * nr ? __ldcg(yb + (long long)b * TB * nr + e) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if (e0 + q * 256 < TB * nr) Yb[e0 + q * 256] = v[q];
+      }
       __syncthreads();
       if (ONE) {
         const double sdot = tile_dot<false, 0>(T, Yb, kb);
@@ -577,11 +587,24 @@ __global__ void solve_gather_bwd(LevelArgs L, LevelArgs PA, int has_parent,
 
 // Load rows [r0, r0 + rows) of a front's x block (columns col0..col0+nr) into Xs
 // [TB][nr], zero-padded; produced rows are read through L2 (__ldcg).
+template <bool ONE>
 __device__ __forceinline__ void load_x_rows(double* Xs, const double* Xf, int r0, int rows,
                                             int nr, int ldr) {
-  for (int e = threadIdx.x; e < TB * nr; e += 256) {
-    const int i = e / nr, j = e - i * nr;
-    Xs[e] = i < rows ? __ldcg(Xf + (long long)(r0 + i) * ldr + j) : 0.0;
+  if (ONE) {  // one column: one load per thread (keeps the one-column kernel's registers low)
+    if (threadIdx.x < TB) Xs[threadIdx.x] = threadIdx.x < rows ? __ldcg(Xf + (long long)(r0 + threadIdx.x) * ldr) : 0.0;
+    return;
+  }
+  const int n = TB * nr;
+  for (int e0 = threadIdx.x; e0 < n; e0 += 8 * 256) {  // eight loads in flight
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int e = e0 + q * 256, i = e / nr, j = e - i * nr;
+      v[q] = (e < n && i < rows) ? __ldcg(Xf + (long long)(r0 + i) * ldr + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      if (e0 + q * 256 < n) Xs[e0 + q * 256] = v[q];
   }
 }
 
@@ -623,7 +646,7 @@ __global__ void __launch_bounds__(256)
         const int r0 = R * TB, rows = min(TB, m - r0);
         tile_fetch(T, Pf + (long long)r0 * kp + j0, kp, rows, kb);
         if (R < nb) wave_wait(flx + f * nb_max + R);
-        load_x_rows(Xs, Xf, r0, rows, nr, ldr);
+        load_x_rows<ONE>(Xs, Xf, r0, rows, nr, ldr);
         cp_async_wait<0>();
         __syncthreads();
         if (ONE) {
@@ -677,16 +700,34 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
         if (tid < kb) Z[tid] += ((red[tid] + red[TB + tid]) + red[2 * TB + tid]) + red[3 * TB + tid];
       } else {
-        for (int e = tid; e < kb * nr; e += 256) {
-          double acc = Z[e];
-          for (int Rq = b + 2; Rq < rt; Rq++)
-            acc += __ldcg(part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB * nr + e);
-          Z[e] = acc;
+        // kb * nr <= 64 * 64: sixteen entries per thread in two halves, the
+        // partials of eight entries requested together (same summation order)
+        const int ne = kb * nr;
+        for (int h = 0; h < TB * kWaveCols; h += 8 * 256) {
+          double acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            const int e = h + tid + q * 256;
+            acc[q] = e < ne ? Z[e] : 0.0;
+          }
+          for (int Rq = b + 2; Rq < rt; Rq++) {
+            const double* pr = part + ((f * rt_max + Rq) * (long long)nb_max + b) * TB * nr;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const int e = h + tid + q * 256;
+              if (e < ne) acc[q] += __ldcg(pr + e);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            const int e = h + tid + q * 256;
+            if (e < ne) Z[e] = acc[q];
+          }
         }
       }
       // (c)
       if (rows1 > 0 && R1 < nb) wave_wait(flx + f * nb_max + R1);
-      load_x_rows(Xs, Xf, R1 * TB, rows1, nr, ldr);
+      load_x_rows<ONE>(Xs, Xf, R1 * TB, rows1, nr, ldr);
       cp_async_wait<0>();
       __syncthreads();
       if (rows1 > 0) {
