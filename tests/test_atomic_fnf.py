@@ -14,6 +14,7 @@ import pytest
 import paper_2306_08994_b200 as tf
 from conftest import golden, golden_names
 from oracle import restate
+from paper_2306_08994_b200.tree import EliminationTree
 
 
 def _plan(g):
@@ -81,3 +82,12 @@ def test_atomic_fnf_cfg2_scale():
         len(st.active) + 2 * len(st.active) ** 2 for st in plan.steps)
     assert s.n_tasks > 7e7 and sum(s.widths) == s.n_tasks
     assert dt < 60
+
+
+def test_atomic_fnf_needs_node_lists():
+    mesh = tf.TensorMesh((8, 8), 1)
+    fronts = tf.sort_fronts(tf.generate_fronts(mesh))
+    tree = EliminationTree(fronts, n_dof=mesh.n_dof, keep_lists=False)
+    plan = tf.symbolic_eliminate(tree, tf.assemble_system(mesh, "one"))
+    with pytest.raises(RuntimeError):
+        tf.compute_atomic_fnf(plan)
