@@ -91,6 +91,40 @@ static int cmp_i32(const void* a, const void* b) {
   return (x > y) - (x < y);
 }
 
+/* one open-addressing table per matrix row x, keyed by column y: the inner
+ * update loop of a pivot walks one row at a time (cache-resident). */
+typedef struct { int32_t* keys; double* vals; int32_t cap, n; } rowmap; /* key y+1, 0 empty */
+
+static int rm_grow(rowmap* r);
+static int32_t rm_slot(rowmap* r, int32_t y, int* fresh) {
+  if ((int64_t)r->n * 10 >= (int64_t)r->cap * 7) { if (rm_grow(r)) return -1; }
+  const int32_t key = y + 1, mask = r->cap - 1;
+  int32_t i = (int32_t)((uint32_t)y * 2654435761u) & mask;
+  while (r->keys[i] && r->keys[i] != key) i = (i + 1) & mask;
+  if (!r->keys[i]) { r->keys[i] = key; r->vals[i] = 0.0; r->n++; *fresh = 1; }
+  else *fresh = 0;
+  return i;
+}
+static int32_t rm_find(const rowmap* r, int32_t y) {
+  if (!r->cap) return -1;
+  const int32_t key = y + 1, mask = r->cap - 1;
+  int32_t i = (int32_t)((uint32_t)y * 2654435761u) & mask;
+  while (r->keys[i] && r->keys[i] != key) i = (i + 1) & mask;
+  return r->keys[i] ? i : -1;
+}
+static int rm_grow(rowmap* r) {
+  const int32_t oc = r->cap, nc = oc ? oc * 2 : 8;
+  int32_t* ok = r->keys; double* ov = r->vals;
+  r->keys = (int32_t*)calloc((size_t)nc, sizeof(int32_t));
+  r->vals = (double*)malloc((size_t)nc * sizeof(double));
+  if (!r->keys || !r->vals) return -1;
+  r->cap = nc; r->n = 0;
+  for (int32_t i = 0; i < oc; i++)
+    if (ok[i]) { int f; int32_t s = rm_slot(r, ok[i] - 1, &f); r->vals[s] = ov[i]; }
+  free(ok); free(ov);
+  return 0;
+}
+
 typedef struct {
   int64_t n_dof, n_piv;
   int32_t* pivot_order;
@@ -149,10 +183,8 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
   if (!R->diag || !R->pivot_order || !R->u_row_ptr || !R->l_col_ptr) return -1;
 
   /* assembly: GlobalSystem.add(ga, gb, E[a][b]) for ga >= gb, element order */
-  cellmap V;
-  if (cm_init(&V, n_elem * (int64_t)nloc * nloc)) return -1;
-  ivec* rows = (ivec*)calloc((size_t)n_dof + 1, sizeof(ivec)); /* cells (z, y) per row z */
-  if (!rows) return -1;
+  rowmap* V = (rowmap*)calloc((size_t)n_dof + 1, sizeof(rowmap)); /* cells (x, y) by row x */
+  if (!V) return -1;
   cellmap A; /* lower-triangle assembled entries */
   if (cm_init(&A, n_elem * (int64_t)nloc * nloc)) return -1;
   int32_t* low_i = NULL; int32_t* low_j = NULL; int64_t n_low = 0, cap_low = 0;
@@ -180,13 +212,13 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
     double v = A.vals[cm_find(&A, (uint32_t)low_i[t], (uint32_t)low_j[t])];
     if (fabs(v) > peak) peak = fabs(v);
     int fresh;
-    int64_t s = cm_slot(&V, (uint32_t)low_i[t], (uint32_t)low_j[t], &fresh);
-    V.vals[s] = v;
-    if (fresh) iv_push(&rows[low_i[t]], low_j[t]);
+    int32_t s = rm_slot(&V[low_i[t]], low_j[t], &fresh);
+    if (s < 0) return -1;
+    V[low_i[t]].vals[s] = v;
     if (low_i[t] != low_j[t]) {
-      s = cm_slot(&V, (uint32_t)low_j[t], (uint32_t)low_i[t], &fresh);
-      V.vals[s] = v;
-      if (fresh) iv_push(&rows[low_j[t]], low_i[t]);
+      s = rm_slot(&V[low_j[t]], low_i[t], &fresh);
+      if (s < 0) return -1;
+      V[low_j[t]].vals[s] = v;
     }
   }
   free(low_i); free(low_j);
@@ -211,6 +243,7 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
   int32_t* cand = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_dof + 1));
   int64_t npiv = 0, node_base = 0, lsize = n_elem;
   ivec rowbuf = {0}, colbuf = {0};
+  double* colv = NULL; double* qv = NULL; int64_t colv_cap = 0;
   for (int32_t L = 0; L < n_levels; L++) {
     /* eligible DOFs of this level, keyed by node */
     int64_t nc = 0;
@@ -231,8 +264,8 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
     free(cnt);
     for (int64_t t = 0; t < nc; t++) {
       const int32_t z = ord[t];
-      const int64_t zs = cm_find(&V, (uint32_t)z, (uint32_t)z);
-      const double pv = zs >= 0 ? V.vals[zs] : 0.0;
+      const int32_t zs = rm_find(&V[z], z);
+      const double pv = zs >= 0 ? V[z].vals[zs] : 0.0;
       if (fabs(pv) <= threshold) {
         R->zp_front = node_base + node_of[z];
         R->zp_pivot = z;
@@ -240,33 +273,47 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
         goto done_zero;
       }
       rowbuf.n = 0; colbuf.n = 0;
-      for (int64_t q = 0; q < rows[z].n; q++) {
-        int32_t y = rows[z].v[q];
-        if (y != z && !elim[y]) iv_push(&rowbuf, y);
+      for (int32_t q = 0; q < V[z].cap; q++) {
+        const int32_t y = V[z].keys[q] - 1;
+        if (y >= 0 && y != z && !elim[y]) iv_push(&rowbuf, y);
       }
       qsort(rowbuf.v, (size_t)rowbuf.n, sizeof(int32_t), cmp_i32);
       /* col = x with (x, z) stored: the pattern is symmetric, so same set as row */
       for (int64_t q = 0; q < rowbuf.n; q++) iv_push(&colbuf, rowbuf.v[q]);
       R->u_row_ptr[npiv] = R->n_u;
+      if (colv_cap < rowbuf.n) {
+        colv_cap = rowbuf.n * 2;
+        colv = (double*)realloc(colv, sizeof(double) * (size_t)colv_cap);
+        qv = (double*)realloc(qv, sizeof(double) * (size_t)colv_cap);
+      }
+      /* Row z and column z are not written while pivot z updates (x, y != z),
+       * so q(z,y) = a(z,y)/a(z,z) and a(x,z) are read once up front, and each
+       * cell a(x,y) still receives exactly a(x,y) - q(z,y)*a(x,z) once per
+       * pivot: the visiting order of distinct cells does not change any
+       * rounding (engine.py:536-545). */
       for (int64_t a = 0; a < rowbuf.n; a++) {
         const int32_t y = rowbuf.v[a];
-        const double qv = V.vals[cm_find(&V, (uint32_t)z, (uint32_t)y)] / pv;
-        push_u(R, z, y, qv);
-        for (int64_t b = 0; b < colbuf.n; b++) {
-          const int32_t x = colbuf.v[b];
-          const double prod = qv * V.vals[cm_find(&V, (uint32_t)x, (uint32_t)z)];
+        qv[a] = V[z].vals[rm_find(&V[z], y)] / pv;
+        push_u(R, z, y, qv[a]);
+      }
+      for (int64_t b = 0; b < colbuf.n; b++)
+        colv[b] = V[colbuf.v[b]].vals[rm_find(&V[colbuf.v[b]], z)];
+      for (int64_t b = 0; b < colbuf.n; b++) {
+        rowmap* row = &V[colbuf.v[b]];
+        const double cx = colv[b];
+        for (int64_t a = 0; a < rowbuf.n; a++) {
+          const double prod = qv[a] * cx;
           int fresh;
-          int64_t s = cm_slot(&V, (uint32_t)x, (uint32_t)y, &fresh);
+          const int32_t s = rm_slot(row, rowbuf.v[a], &fresh);
           if (s < 0) return -1;
-          if (fresh) iv_push(&rows[x], y);
-          V.vals[s] = V.vals[s] - prod;
+          row->vals[s] = row->vals[s] - prod;
         }
       }
       R->diag[z] = pv;
       R->l_col_ptr[npiv] = R->n_l;
       for (int64_t b = 0; b < colbuf.n; b++) {
         const int32_t x = colbuf.v[b];
-        push_l(R, x, z, V.vals[cm_find(&V, (uint32_t)x, (uint32_t)z)] / pv);
+        push_l(R, x, z, V[x].vals[rm_find(&V[x], z)] / pv);
       }
       R->pivot_order[npiv++] = z;
       elim[z] = 1;
@@ -279,11 +326,10 @@ int oracle_factor(int64_t n_dof, int64_t n_elem, int32_t nloc, const int32_t* do
   R->l_col_ptr[npiv] = R->n_l;
 done_zero:
   R->n_piv = npiv;
-  free(rowbuf.v); free(colbuf.v);
+  free(rowbuf.v); free(colbuf.v); free(colv); free(qv);
   free(lp); free(leaf); free(elim); free(node_of); free(cand);
-  for (int64_t g = 0; g <= n_dof; g++) free(rows[g].v);
-  free(rows);
-  free(V.keys); free(V.vals);
+  for (int64_t g = 0; g <= n_dof; g++) { free(V[g].keys); free(V[g].vals); }
+  free(V);
   return R->zp_pivot >= 0 ? 2 : 0;
 }
 

@@ -107,6 +107,58 @@ class FactorResult:
                     u[(z, z)] = float(P[c, c])
         return u, l
 
+    def _lookup(self, piv: np.ndarray, row: np.ndarray) -> np.ndarray:
+        """Stored factor entry (row `row`, pivot column `piv`), global 1-based indices.
+
+        Vectorised over key arrays; needs a plan built with node lists.  The
+        entry is l(row, piv) = u(piv, row) (LDL^T), or the pivot d when row == piv.
+        """
+        plan, dp = self.plan, self.device_plan
+        native = plan.native
+        piv = np.asarray(piv, dtype=np.int64).ravel()
+        row = np.asarray(row, dtype=np.int64).ravel()
+        inv = np.full(self.n_dof + 1, -1, dtype=np.int64)
+        inv[native.pivot_order.astype(np.int64)] = np.arange(native.n_pivots, dtype=np.int64)
+        pos = inv[piv]
+        if np.any(pos < 0):
+            raise KeyError("key column is not a pivot")
+        bases = np.array([lt.piv_base for lt in native.levels], dtype=np.int64)
+        lev = np.searchsorted(bases, pos, side="right") - 1
+        out = np.empty(len(piv), dtype=np.float64)
+        for L in np.unique(lev):
+            sel = np.nonzero(lev == L)[0]
+            lt, dl = native.levels[int(L)], dp.levels[int(L)]
+            ptr, _, idx = native.node_lists(int(L))
+            f = np.searchsorted(lt.piv_off, pos[sel], side="right") - 1
+            col = pos[sel] - lt.piv_off[f]
+            kp = lt.pat[lt.pattern_of[f], _lib.PAT_KP].astype(np.int64)
+            r = np.empty(len(sel), dtype=np.int64)
+            for t, (ff, g) in enumerate(zip(f, row[sel])):
+                hit = np.nonzero(idx[ptr[ff]:ptr[ff + 1]] == g)[0]
+                if len(hit) != 1:
+                    raise KeyError((int(g), int(piv[sel[t]])))
+                r[t] = hit[0]
+            if np.any(r < col):
+                raise KeyError("key is above the diagonal of its front")
+            flat = torch.from_numpy(f * dl.fac_stride + r * kp + col).to(dp.device)
+            out[sel] = dp.factors[int(L)][flat].cpu().numpy()
+        return out
+
+    def u_values(self, keys) -> np.ndarray:
+        """u(z, y) for an (n, 2) array of keys, without building the dictionaries."""
+        k = np.asarray(keys, dtype=np.int64).reshape(-1, 2)
+        return self._lookup(k[:, 0], k[:, 1])
+
+    def l_values(self, keys) -> np.ndarray:
+        """l(x, z) for an (n, 2) array of keys, without building the dictionaries."""
+        k = np.asarray(keys, dtype=np.int64).reshape(-1, 2)
+        return self._lookup(k[:, 1], k[:, 0])
+
+    def pivot_values(self, positions) -> np.ndarray:
+        """d at the given pivot-order positions."""
+        po = self.plan.native.pivot_order.astype(np.int64)[np.asarray(positions, dtype=np.int64)]
+        return self._lookup(po, po)
+
     @property
     def u_entries(self) -> dict[tuple[int, int], float]:
         return self._dicts[0]

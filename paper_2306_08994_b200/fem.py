@@ -270,14 +270,33 @@ class FrontSet(Sequence):
     (membership computed like generate_fronts, fem.py:241-255).
     """
 
-    def __init__(self, dofs, values, front_ids=None, ptr=None):
+    def __init__(self, dofs, values, front_ids=None, ptr=None, membership=None):
         self.ptr = None if ptr is None else np.ascontiguousarray(ptr, dtype=np.int64)
         self.dofs = np.ascontiguousarray(dofs, dtype=np.int32)
         self.values = np.ascontiguousarray(values, dtype=np.float64)
         n = len(self.ptr) - 1 if self.ptr is not None else self.dofs.shape[0]
         self.front_ids = (np.arange(n, dtype=np.int64) if front_ids is None
                           else np.ascontiguousarray(front_ids, dtype=np.int64))
+        # explicit per-entry membership (from user Fronts), else derived from the set
+        self.membership = (None if membership is None
+                           else np.ascontiguousarray(membership, dtype=np.int32).reshape(self.dofs.shape))
         self._n = n
+        self._counts = None
+
+    def membership_of(self, i: int) -> np.ndarray:
+        """Per-index membership of front i.
+
+        generate_fronts (fem.py:241-250) marks an index with the number of
+        leaf fronts that hold it (2 at shared 1D endpoints, 1 elsewhere); the
+        same count is used for 2D/3D element sets.  Fronts built by the caller
+        keep the membership they were given.
+        """
+        if self.membership is not None:
+            return self.membership[i] if self.ptr is None else \
+                self.membership[self.ptr[i]:self.ptr[i + 1]]
+        if self._counts is None:
+            self._counts = np.bincount(self.dofs.ravel().astype(np.int64)).astype(np.int32)
+        return self._counts[self.dofs_of(i)]
 
     @property
     def uniform_values(self) -> bool:
@@ -312,19 +331,32 @@ class FrontSet(Sequence):
             raise IndexError(i)
         idx = tuple(int(g) for g in self.dofs_of(i))
         n = len(idx)
-        return Front(front_id=int(self.front_ids[i]), indices=idx, membership=(1,) * n,
-                     computed=(False,) * n, values=np.array(self.values_of(i), copy=True))
+        vals = self.values_of(i)
+        if getattr(self, "padded_values", False):
+            vals = vals[:n, :n]
+        return Front(front_id=int(self.front_ids[i]), indices=idx,
+                     membership=tuple(int(c) for c in self.membership_of(i)),
+                     computed=(False,) * n, values=np.array(vals, copy=True))
 
     def take(self, order: np.ndarray) -> "FrontSet":
         order = np.asarray(order, dtype=np.int64)
         vals = self.values if self.uniform_values else self.values[order]
         if self.ptr is None:
-            return FrontSet(self.dofs[order], vals, self.front_ids[order])
+            mem = None if self.membership is None else self.membership[order]
+            out = FrontSet(self.dofs[order], vals, self.front_ids[order], membership=mem)
+            out._counts = self._counts
+            return out
         sizes = np.diff(self.ptr)[order]
         ptr = np.concatenate([[0], np.cumsum(sizes)])
         flat = np.concatenate([self.dofs_of(int(i)) for i in order]) if len(order) else \
             np.zeros(0, np.int32)
-        return FrontSet(flat, vals, self.front_ids[order], ptr=ptr)
+        mem = None
+        if self.membership is not None:
+            mem = np.concatenate([self.membership_of(int(i)) for i in order]) if len(order) else \
+                np.zeros(0, np.int32)
+        out = FrontSet(flat, vals, self.front_ids[order], ptr=ptr, membership=mem)
+        out.padded_values = getattr(self, "padded_values", False)
+        return out
 
     @classmethod
     def from_fronts(cls, fronts: Sequence[Front]) -> "FrontSet":
@@ -339,14 +371,16 @@ class FrontSet(Sequence):
             v0 = fronts[0].values
             same = all(np.array_equal(f.values, v0) for f in fronts)
             vals = v0 if same else np.stack([f.values for f in fronts])
-            return cls(dofs, vals, ids)
+            mem = np.array([f.membership for f in fronts], dtype=np.int32)
+            return cls(dofs, vals, ids, membership=mem)
         ptr = np.concatenate([[0], np.cumsum(sizes)])
         flat = np.array([g for f in fronts for g in f.indices], dtype=np.int32)
         raise_if = max(sizes)
         vals = np.zeros((len(fronts), raise_if, raise_if))
         for i, f in enumerate(fronts):
             vals[i, :f.size, :f.size] = f.values
-        fs = cls(flat, vals, ids, ptr=ptr)
+        mem = np.array([c for f in fronts for c in f.membership], dtype=np.int32)
+        fs = cls(flat, vals, ids, ptr=ptr, membership=mem)
         fs.padded_values = True
         return fs
 

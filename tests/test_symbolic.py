@@ -58,6 +58,30 @@ def test_membership_and_nodes_n2():
     assert tree.nodes[tree.root_id].front.indices == (1, 2, 3)
 
 
+def test_generate_fronts_membership_kats():
+    """SPEC.md:90-92 (fem.py:241-250): shared endpoints count 2, others 1."""
+    fr = tf.generate_fronts(tf.Mesh(2, 1))
+    assert [f.membership for f in fr] == [(1, 2), (2, 1)]
+    assert [f.membership for f in tf.generate_fronts(tf.Mesh(1, 3))] == [(1, 1, 1, 1)]
+    assert [f.membership for f in tf.generate_fronts(tf.Mesh(3, 2))] == \
+        [(1, 1, 2), (2, 1, 2), (2, 1, 1)]
+    # against the reference's own generate_fronts for every 1D golden mesh
+    for name in golden_names():
+        g = golden(name)
+        if len(g["dims"]) != 1:
+            continue
+        n, p = int(g["dims"][0]), int(g["degree"])
+        mem = [f.membership for f in tf.generate_fronts(tf.Mesh(n, p))]
+        ref = [(1 if e == 0 else 2,) + (1,) * (p - 1) + (1 if e == n - 1 else 2,) for e in range(n)]
+        assert mem == ref
+    # sorting keeps it; 2D/3D: number of elements holding the DOF
+    f2 = tf.sort_fronts(tf.generate_fronts(tf.TensorMesh((2, 2), 1)))
+    assert sorted(f2[0].membership) == [1, 2, 2, 4]
+    # caller-built fronts keep their own membership
+    user = tf.Front(0, (1, 2), (3, 1), (False, False), np.eye(2))
+    assert tf.build_elimination_tree([user]).fronts[0].membership == (3, 1)
+
+
 def test_element_and_assembly_kats():
     """SPEC.md:63, 73, 81."""
     assert np.allclose(tf.element_mass_matrix(1.0, 1), np.array([[2, 1], [1, 2]]) / 6, atol=1e-16)
