@@ -6,7 +6,8 @@ device-resident inputs.  Symbolic planning is excluded from the timed region,
 as in the reference's own timing window (cli.py:153-161).
 
   python bench.py [--config cfg5] [--gpus N] [--steps K] [--warmup W]
-  python bench.py --impl reference ...   (the reference's CPU arithmetic, oracle port)
+  python bench.py --impl reference ...   (the reference's arithmetic on the host cores:
+                                          oracle/cpu_baseline.py, no product import)
 
 Prints ONE JSON line on rank 0.
 """
@@ -43,7 +44,6 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "cfg5"
 FP64_PEAK_TFLOPS = 35.47  # measured cuBLAS DGEMM on this pool: profiles/r01_dgemm_cublas_peak.log
-CPU_SAMPLE = dict(shape=(128, 128), degree=1)
 
 
 def measured_traffic(config, kernel):
@@ -113,52 +113,59 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU baseline
-def cpu_sample_rate(target_lu_flops: float, target_n_dof: int):
-    """Reference arithmetic (C port of engine.py:500-552 + 468-493, 1 thread) on a
-    bounded sample: the 2D Q1 128x128 sub-problem; DoF/s extrapolated to the
-    workload by the reference's LU task count."""
-    import paper_2306_08994_b200 as tf
-    from oracle.tfo import OracleFactors
-    mesh = tf.TensorMesh(CPU_SAMPLE["shape"], CPU_SAMPLE["degree"])
-    fr = tf.generate_fronts(mesh)
-    plan = tf.symbolic_eliminate(tf.build_elimination_tree(fr, n_dof=mesh.n_dof))
-    lu = sum(s["lu_flops"] for s in plan.level_stats())
-    b = np.random.default_rng(0).standard_normal(mesh.n_dof)
-    t0 = time.perf_counter()
-    o = OracleFactors(mesh.n_dof, fr.dofs, fr.values)
-    o.solve(b)
-    dt = time.perf_counter() - t0
-    t_target = dt * target_lu_flops / lu
-    return {"value": target_n_dof / t_target, "unit": "DoF/s", "cores": 1, "kind": "port",
-            "sample": (f"full factor+solve of 2D Q1 128x128 ({mesh.n_dof} DoF, {lu:.3e} LU "
-                       f"task-flops) in {dt:.2f}s with the reference's cell-level arithmetic "
-                       f"(oracle/tf_oracle.c, 1 thread); extrapolated to the workload's "
-                       f"{target_lu_flops:.3e} task-flops"),
-            "sample_seconds": dt}
+def cpu_baseline(args) -> dict:
+    """The reference arm's measurement (below) run once in a fresh interpreter
+    (no torch / CUDA state is forked), on rank 0 at N=1."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", args.config,
+           "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, cwd=str(ROOT),
+                         env={k: v for k, v in os.environ.items()
+                              if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+    if out.returncode != 0:
+        return {"error": out.stderr[-500:]}
+    return json.loads(out.stdout.strip().splitlines()[-1])["cpu_baseline"]
 
 
 # ------------------------------------------------------------------ reference
 def run_reference(args, cfg):
+    """The reference's arithmetic on the host cores (oracle/cpu_baseline.py).
+
+    Imports nothing from the product package.  ms_per_step is the measured
+    wall time of one step (one factor+solve of the sample per core); value is
+    the workload's DoF/s (measured when the sample is the workload, cfg1 /
+    cfg2; else extrapolated by the workload's exact reference task count)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    tf, mesh, fronts, system, plan = build_problem(cfg)
-    lu = sum(s["lu_flops"] for s in plan.level_stats())
+    from oracle import cpu_baseline as cb
+    sshape = cb.sample_shape(cfg["shape"], cfg["degree"])
+    # the reference solves one column per call (engine.py:471-472): the sample solves
+    # min(nrhs, 4) columns and the solve time scales to the workload's nrhs
+    sample = cb.Sample(sshape, cfg["degree"], nrhs=min(cfg["nrhs"], 4))
+    procs, rss = cb.choose_procs(sample)
     for _ in range(args.warmup):
-        r = cpu_sample_rate(lu, mesh.n_dof)
-    vals = []
+        cb.run_step(sample, procs)
+    walls, per = [], []
+    t_start = time.perf_counter()
     for _ in range(args.steps):
-        r = cpu_sample_rate(lu, mesh.n_dof)
-        vals.append(r["value"])
-    v = float(np.mean(vals))
+        w, p, _ = cb.run_step(sample, procs)
+        walls.append(w)
+        per.extend(p)
+    t_total = time.perf_counter() - t_start
+    wall = float(np.mean(walls))
+    base = cb.describe(cfg["shape"], cfg["degree"], cfg["nrhs"], sample, procs, wall, per)
+    base["max_rss_bytes_per_process"] = int(rss)
+    v = base["value"]
     line = {"metric": "factor+solve DoF/s", "value": v, "unit": "DoF/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mesh.n_dof / v * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "label": cfg["label"], "n_dof": mesh.n_dof,
-                       "nrhs": cfg["nrhs"]},
-            "cpu_baseline": {"value": v, "unit": "DoF/s", "cores": 1, "kind": "port",
-                             "sample": r["sample"]},
+            "config": {"workload": args.config, "label": cfg["label"],
+                       "n_dof": int(np.prod([x * cfg["degree"] + 1 for x in cfg["shape"]])),
+                       "nrhs": cfg["nrhs"], "sample_shape": list(sshape),
+                       "value_basis": base["value_basis"]},
+            "timed_seconds_total": t_total,
+            "cpu_baseline": base,
             "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -379,7 +386,7 @@ def run_ours(args, cfg):
         "kernel_ms_per_step": kernel_ms,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_sample_rate(sum(s["lu_flops"] for s in stats), n)
+        line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -29,6 +29,8 @@ from .fem import (
 )
 from .tree import EliminationTree, TreeNode, build_elimination_tree, join_fronts, sort_fronts
 from .symbolic import EliminationPlan, NodeReorder, PivotStep, symbolic_eliminate
+from .tasks import (DagReport, DependencyGraph, Task, build_dependency_edges, build_task_graph,
+                    enumerate_tasks, validate_dag)
 from .schedule import (AtomicFoataSchedule, FoataSchedule, TaskKind, compute_atomic_fnf,
                        compute_fnf, schedule_stats, schedule_stats_csv)
 from .engine import (

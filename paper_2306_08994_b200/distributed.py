@@ -157,6 +157,9 @@ class TorchComm:
     def allreduce_sum(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
 
+    def broadcast(self, t, src: int):
+        self.dist.broadcast(t, src, group=self.group)
+
     def allreduce_min(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
 
@@ -291,6 +294,32 @@ class ShardedFactorization:
                         self.state[r].fac[L][:(f1 - f0) * dl.fac_stride]
             out.append(full)
         return out
+
+    def gather_all(self) -> None:
+        """Give every process the complete factorization in `dp`'s one-GPU layout.
+
+        Each level's owned front ranges (factor panels and, on large levels,
+        the diagonal-block inverses the solve reads) are broadcast from their
+        owner, so `dp.solve_into` and the factor dictionaries then work on any
+        rank without further communication.  Collective over the group.
+        """
+        dp = self.dp
+        me = None if isinstance(self.comm, LocalComm) else self.ranks[0]
+        for L, dl in enumerate(dp.levels):
+            parts = [(dp.factors[L], dl.fac_stride, "fac")]
+            if dl.aux is not None:
+                parts.append((dl.aux, dl.aux_stride, "aux"))
+            for full, stride, kind in parts:
+                for r in range(self.world):
+                    f0, f1 = self.shard.levels[L].ranges[r]
+                    if f1 <= f0:
+                        continue
+                    dst = full[f0 * stride:f1 * stride]
+                    if r in self.state:
+                        src = self.state[r].fac[L] if kind == "fac" else self.state[r].aux[L]
+                        dst.copy_(src[:(f1 - f0) * stride])
+                    if me is not None:
+                        self.comm.broadcast(dst, r)
 
     # ---------------------------------------------------------------- solve
     def _solve_slots(self, r: int, L: int):

@@ -196,28 +196,56 @@ def _factorize(plan, state: ExecState, compiled: Optional[DevicePlan] = None) ->
     return res
 
 
+def _plan_of(x):
+    """EliminationPlan of a plan or of a DependencyGraph (graph.plan, tasks.py:185-204)."""
+    return getattr(x, "plan", x) if not hasattr(x, "native") else x
+
+
 def run_sequential(plan, state: ExecState) -> FactorResult:
-    """Execute the level classes in order on the current CUDA stream (engine.py:177-184)."""
-    plan = getattr(plan, "plan", plan)  # accept a DependencyGraph-like wrapper
-    return _factorize(plan, state)
+    """Execute the level classes in order on the current CUDA stream (engine.py:177-184).
+
+    Accepts the reference's DependencyGraph (cli.py:157) or an EliminationPlan."""
+    return _factorize(_plan_of(plan), state)
 
 
 def run_concurrent(schedule, plan, state: ExecState, workers: int = 1, debug: bool = False,
                    compiled: Optional[DevicePlan] = None) -> FactorResult:
     """Execute classes in order with a barrier between classes (engine.py:354-419).
 
-    Within a class the GPU runs every front concurrently; the stream order
-    between level launches is the barrier.  `workers` > 1 with an initialised
-    torch.distributed group shards independent subtrees across GPUs
-    (paper_2306_08994_b200.distributed); with a single process it only
-    validates the argument like the reference.
+    Within a class the GPU runs every front concurrently and the stream order
+    between level launches is the class barrier.  The reference's `workers`
+    are CPU processes sharing one matrix; here the unit of concurrency is a
+    GPU.  workers == 1 runs on the current device.  workers > 1 requires an
+    initialised torch.distributed group of exactly `workers` ranks (one per
+    GPU; NCCL on a GPU box): the tree is sharded by subtrees
+    (distributed.ShardedFactorization) and every rank
+    returns the same FactorResult (factors gathered, bitwise equal to the
+    one-GPU run).  Without such a group, workers > 1 raises ValueError rather
+    than silently running on one GPU.
     """
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
+    plan = _plan_of(plan)
     if debug:
         from .verify import check_level_schedule
         check_level_schedule(plan, schedule)
-    return _factorize(plan, state, compiled)
+    if workers == 1:
+        return _factorize(plan, state, compiled)
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() != workers:
+        raise ValueError(f"workers={workers} needs an initialised torch.distributed group of "
+                         f"{workers} ranks (one per GPU)")
+    from .distributed import ShardedFactorization, TorchComm
+    dp = compiled or state.compiled or compile_execution(plan, None, state)
+    sf = ShardedFactorization(dp, workers, TorchComm(), ranks=[dist.get_rank()])
+    pos = sf.factor(state.zero_threshold)
+    if pos >= 0:
+        front, pivot = plan.locate_pivot(pos)
+        raise ZeroPivotError(front, pivot)
+    sf.gather_all()
+    res = FactorResult(plan, dp)
+    state.factors = res
+    return res
 
 
 def factorize(plan, system) -> FactorResult:

@@ -9,7 +9,8 @@ class(L) = 1 + max class(children) = L + 1.  Every atomic J-edge of the
 reference goes from a level to the same or a later level, so executing the
 level classes in order (one GPU launch sequence per class, stream order as
 the barrier) is a valid linearization of the reference's Diekert graph
-(checked against the atomic graph in tests/test_schedule.py).
+(every J1-J4 edge of the restated atomic graph is level-nondecreasing:
+tests/test_schedule.py).
 """
 
 from __future__ import annotations
@@ -55,8 +56,19 @@ class ScheduleStats:
     mixed_classes: tuple[int, ...]
 
 
-def compute_fnf(plan) -> FoataSchedule:
-    """Canonical FNF of the front-granularity trace (levels of the tree)."""
+def compute_fnf(plan_or_graph):
+    """Canonical FNF (schedule.py:60-82).
+
+    Given a `DependencyGraph` (the reference's call, cli.py:149) this is the
+    FNF of the atomic trace, as statistics (`AtomicFoataSchedule`: class
+    widths and kind sets equal the reference's).  Given an `EliminationPlan`
+    it is the FNF of the front-granularity trace the GPU executes: one class
+    per tree level.
+    """
+    from .tasks import DependencyGraph
+    if isinstance(plan_or_graph, DependencyGraph):
+        return compute_atomic_fnf(plan_or_graph.plan)
+    plan = plan_or_graph
     native = plan.native
     kinds = []
     for lt in native.levels:

@@ -17,8 +17,14 @@ from .errors import ContractViolationError
 
 
 def check_level_schedule(plan, schedule) -> None:
+    from .schedule import AtomicFoataSchedule
     native = plan.native
-    if schedule is not None and tuple(schedule.level_sizes) != tuple(plan.tree.level_sizes):
+    if isinstance(schedule, AtomicFoataSchedule):
+        # the atomic FNF of the same plan: its task count must be the plan's
+        st = native.atomic_fnf()[0] if native.keep_lists else None
+        if st is not None and int(st.n_tasks) != sum(schedule.widths):
+            raise ContractViolationError("atomic schedule does not belong to this plan")
+    elif schedule is not None and tuple(schedule.level_sizes) != tuple(plan.tree.level_sizes):
         raise ContractViolationError("schedule classes do not match the tree levels")
     for L, lt in enumerate(native.levels):
         if L > 0 and lt.n_fronts != (native.levels[L - 1].n_fronts + 1) // 2:
