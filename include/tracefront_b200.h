@@ -165,8 +165,11 @@ typedef struct {
  * shared-memory / large-front split (0 for shared-memory levels). */
 int64_t tf_level_aux_doubles(const tf_level_view* lv);
 
-/* Workspace bytes tf_level_factor / tf_level_solve_* need for this level with
- * nrhs right-hand sides (0 when none). */
+/* Workspace bytes tf_level_factor may use for this level (0 when none): the
+ * root-dataflow kernel's acquire/release flags.  Passing a caller-owned
+ * workspace of this size keeps concurrent factorizations (different plans /
+ * streams) from sharing flags; with workspace == NULL a per-device scratch
+ * buffer is used. */
 int64_t tf_level_factor_workspace(const tf_level_view* lv);
 
 /* One Foata class (tree level) of the numeric factorization: extend-add of

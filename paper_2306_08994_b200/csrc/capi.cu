@@ -9,7 +9,8 @@ cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, con
                                 unsigned long long* err, cudaStream_t st);
 cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, double* factors,
                                 double* upd_out, double thr, unsigned long long* err,
-                                cudaStream_t st);
+                                int* ws_flags, cudaStream_t st);
+bool root_dataflow_level(const LevelArgs& L);
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
                              long long out_rows, double* y, int nrhs, double* work,
@@ -44,8 +45,11 @@ extern "C" int64_t tf_level_aux_doubles(const tf_level_view* lv) {
 }
 
 extern "C" int64_t tf_level_factor_workspace(const tf_level_view* lv) {
-  (void)lv;
-  return 0;
+  // the root-dataflow kernel's acquire/release flags: one set per caller-owned
+  // workspace, so concurrent factorizations never share them
+  if (!lv || lv->n_fronts == 0 || !level_is_large(lv->is_leaf, lv->max_m)) return 0;
+  const LevelArgs L = make_args(lv);
+  return root_dataflow_level(L) ? (int64_t)sizeof(int) * root_flag_ints(L) : 0;
 }
 
 extern "C" int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs) {
@@ -57,8 +61,6 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
                                const double* elem, double* factors, double* upd_out,
                                double threshold, unsigned long long* err, void* workspace,
                                int64_t workspace_bytes, void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   if (!lv || !err) return TF_ERR_INVALID;
   if (lv->n_fronts == 0) return TF_OK;
   if (lv->is_leaf && !elem) return TF_ERR_INVALID;
@@ -69,7 +71,12 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
     return status(launch_factor_small(L, child_upd, elem, factors, upd_out, threshold, err, st));
   if (lv->max_k > 0 && (!lv->aux || lv->aux_stride < large_aux_doubles(lv->max_k)))
     return TF_ERR_INVALID;
-  return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, st));
+  int* flags = nullptr;
+  if (workspace) {
+    if (workspace_bytes < tf_level_factor_workspace(lv)) return TF_ERR_INVALID;
+    flags = static_cast<int*>(workspace);
+  }
+  return status(launch_factor_large(L, child_upd, factors, upd_out, threshold, err, flags, st));
 }
 
 extern "C" int32_t tf_subtree_fusable(const tf_level_view* views, int32_t n_levels) {

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <utility>
 
 #include "tracefront_b200.h"
 
@@ -17,6 +18,28 @@ extern int g_small_max_m;
 // Per-front doubles of the diagonal-block inverses a large-front level keeps.
 long long large_aux_doubles(int max_k);
 inline bool level_is_large(int is_leaf, int max_m) { return !is_leaf && max_m > g_small_max_m; }
+
+// Persistent kernels whose CTAs wait on each other (wavefront solves, root
+// dataflow) are launched cooperatively: the runtime either makes the whole
+// grid co-resident or fails the launch (cudaErrorCooperativeLaunchTooLarge),
+// so a spin-wait can never depend on a CTA that is not scheduled (MPS,
+// concurrent kernels).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cooperative(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                      cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 
 // Kernel classes for the optional launch timing (timing.cu).
 enum KernelClass {
@@ -76,6 +99,12 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.child_base = v->child_base;
   a.level_fronts = v->level_fronts > 0 ? v->level_fronts : v->n_fronts;
   return a;
+}
+
+// Root-dataflow flag words of a level (factor workspace, tf_level_factor_workspace)
+inline long long root_flag_ints(const LevelArgs& L) {
+  const long long T = (L.max_k + 63) / 64, nf = L.n_fronts;
+  return nf * T * T + 2 * nf * T + 1 + nf;
 }
 
 // Per-front view of the pattern row.

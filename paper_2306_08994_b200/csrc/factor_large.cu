@@ -907,8 +907,11 @@ struct LookaheadStreams {
   cudaStream_t chain = nullptr, panel = nullptr, schur = nullptr;
   cudaEvent_t start, chain_done, panel_done, schur_done;
 };
-static LookaheadStreams& lookahead_streams() {
-  static LookaheadStreams ls;
+static LookaheadStreams& lookahead_streams() {  // one set per device
+  static LookaheadStreams all[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LookaheadStreams& ls = all[dev & 63];
   if (!ls.chain) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -988,6 +991,10 @@ static bool root_dataflow() {  // TFB_ROOT_DATAFLOW=0 selects the lookahead path
     v = e ? atoi(e) != 0 : 1;
   }
   return v != 0;
+}
+
+bool root_dataflow_level(const LevelArgs& L) {
+  return L.max_upd == 0 && L.max_k > 0 && root_dataflow();
 }
 
 // ------------------------------------------------------------- root fronts
@@ -1415,11 +1422,12 @@ static int* root_flags(long long ints) {  // per-device scratch, grown on demand
 }
 
 static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
-                               unsigned long long* err, cudaStream_t st) {
+                               unsigned long long* err, int* ws_flags, cudaStream_t st) {
   const int T = (L.max_k + NB - 1) / NB;
   const long long nf = L.n_fronts;
-  const long long nflags = nf * T * T + 2 * nf * T + 1 + nf;
-  int* flags = root_flags(nflags);
+  const long long nflags = root_flag_ints(L);
+  // the caller's workspace (one per DevicePlan level), else a per-device scratch
+  int* flags = ws_flags ? ws_flags : root_flags(nflags);
   if (!flags) return cudaErrorMemoryAllocation;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * nflags, st);
   if (e != cudaSuccess) return e;
@@ -1445,8 +1453,10 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
     cudaMemset(trace, 0, sizeof(long long) * 8 * 4096);
   }
   timer_begin(K_ROOT, st);
-  large_root_kernel<<<grid, 256, kRootSmem, st>>>(L, factors, thr, err, flags, T, trace);
+  e = launch_cooperative(large_root_kernel, dim3(grid), dim3(256), kRootSmem, st, L, factors, thr,
+                         err, flags, T, trace);
   timer_end(st);
+  if (e != cudaSuccess) return e;
   if (trace && T <= 4096) {
     static std::vector<long long> h;
     h.resize(8 * T);
@@ -1462,7 +1472,7 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
 }
 
 cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, double* factors,
-                                double* upd_out, double thr, unsigned long long* err,
+                                double* upd_out, double thr, unsigned long long* err, int* ws_flags,
                                 cudaStream_t st) {
   if (L.is_leaf) return cudaErrorInvalidValue;  // element fronts are never this large
   if (L.max_k > 0 && (!L.aux || L.aux_stride < large_aux_doubles(L.max_k)))
@@ -1495,7 +1505,7 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (L.max_upd == 0 && L.max_k > 0 && root_dataflow())
-    return factor_root(L, factors, thr, err, st);
+    return factor_root(L, factors, thr, err, ws_flags, st);
   if (lookahead) return factor_lookahead(L, child_upd, factors, upd_out, thr, err, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);

@@ -1731,18 +1731,20 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr);
     if (nb > 0) cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb, st);
     timer_begin(K_SOLVE_FWD_WAVE, st);
+    cudaError_t e;
     if (nr == 1) {
       const unsigned g = wave_grid(solve_fwd_wave<true>, smem, (long long)rt * L.n_fronts);
-      solve_fwd_wave<true><<<g, 256, smem, st>>>(L, C, child_at0, factors, w_child, child_rows,
-                                                  w_out, out_rows, y, nr, nrhs, col0, flags, yblk,
-                                                  nb, rt, nbuf);
+      e = launch_cooperative(solve_fwd_wave<true>, dim3(g), dim3(256), smem, st, L, C, child_at0,
+                             factors, w_child, child_rows, w_out, out_rows, y, nr, nrhs, col0,
+                             flags, yblk, nb, rt, nbuf);
     } else {
       const unsigned g = wave_grid(solve_fwd_wave<false>, smem, (long long)rt * L.n_fronts);
-      solve_fwd_wave<false><<<g, 256, smem, st>>>(L, C, child_at0, factors, w_child, child_rows,
-                                                   w_out, out_rows, y, nr, nrhs, col0, flags,
-                                                   yblk, nb, rt, nbuf);
+      e = launch_cooperative(solve_fwd_wave<false>, dim3(g), dim3(256), smem, st, L, C, child_at0,
+                             factors, w_child, child_rows, w_out, out_rows, y, nr, nrhs, col0,
+                             flags, yblk, nb, rt, nbuf);
     }
     timer_end(st);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -1814,16 +1816,18 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
     const size_t smem = sizeof(double) * (nbuf * TB * TLD + 2 * TB * nr + 4 * TB);
     cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)L.n_fronts * nb * (1 + rt), st);
     timer_begin(K_SOLVE_BWD_WAVE, st);
+    cudaError_t e;
     if (nr == 1) {
       const unsigned g = wave_grid(solve_bwd_wave<true>, smem, ntiles);
-      solve_bwd_wave<true><<<g, 256, smem, st>>>(L, factors, x_out, out_rows, y, nr, nrhs, col0,
-                                                  flags, part, nb, rt, nbuf);
+      e = launch_cooperative(solve_bwd_wave<true>, dim3(g), dim3(256), smem, st, L, factors, x_out,
+                             out_rows, y, nr, nrhs, col0, flags, part, nb, rt, nbuf);
     } else {
       const unsigned g = wave_grid(solve_bwd_wave<false>, smem, ntiles);
-      solve_bwd_wave<false><<<g, 256, smem, st>>>(L, factors, x_out, out_rows, y, nr, nrhs, col0,
-                                                   flags, part, nb, rt, nbuf);
+      e = launch_cooperative(solve_bwd_wave<false>, dim3(g), dim3(256), smem, st, L, factors, x_out,
+                             out_rows, y, nr, nrhs, col0, flags, part, nb, rt, nbuf);
     }
     timer_end(st);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

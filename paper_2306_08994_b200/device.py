@@ -99,6 +99,11 @@ class DeviceLevel:
             v.aux = self.aux.data_ptr()
             v.aux_stride = self.aux_stride
         self.view = v
+        # factor scratch owned by this plan (root-dataflow flags): concurrent
+        # factorizations of different plans never share it
+        self.ws_bytes = int(lib.tf_level_factor_workspace(C.byref(v)))
+        self.ws = (torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+                   if self.ws_bytes > 0 else None)
 
     @property
     def large(self) -> bool:
@@ -106,14 +111,14 @@ class DeviceLevel:
 
 
 class DevicePlan:
-    def __init__(self, plan, fronts, device: Optional[torch.device] = None):
+    def __init__(self, plan, fronts, device: Optional[torch.device] = None, values=None):
         self.device = device or require_cuda()
         self.lib = _lib.load()
         self.plan = plan
         native = plan.native
         self.n_dof = plan.n_dof
         self.n_pivots = native.n_pivots
-        vals = np.ascontiguousarray(fronts.values, dtype=np.float64)
+        vals = np.ascontiguousarray(fronts.values if values is None else values, dtype=np.float64)
         elem_ld = vals.shape[-1]
         elem_stride = 0 if vals.ndim == 2 else elem_ld * elem_ld
         self.elem = torch.from_numpy(vals.ravel()).to(self.device)
@@ -154,7 +159,8 @@ class DevicePlan:
         prev = self.upd[(L - 1) & 1] if L > 0 else None
         rc = self.lib.tf_level_factor(C.byref(dl.view), _ptr(prev), _ptr(self.elem),
                                       _ptr(self.factors[L]), _ptr(self.upd[L & 1]),
-                                      C.c_double(threshold), _ptr(self.err), None, 0, sp)
+                                      C.c_double(threshold), _ptr(self.err), _ptr(dl.ws),
+                                      dl.ws_bytes, sp)
         _lib.check(rc, f"tf_level_factor(level {L})")
 
     @property
@@ -253,6 +259,32 @@ class DevicePlan:
             prev = cur
         _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(y), _ptr(x), nrhs, 1,
                                        sp), "tf_permute_rows")
+
+    def capture(self, threshold: float, b: torch.Tensor, x: torch.Tensor,
+                warmup: bool = True) -> "torch.cuda.CUDAGraph":
+        """One CUDA graph of a whole factorization + solve (every level's
+        launches, the lookahead streams' fork/join, the wavefront sweeps).
+
+        `b` and `x` are the static right-hand-side / solution buffers and
+        `self.elem` the static leaf values: update them in place, then
+        `graph.replay()`.  Removes the per-launch host cost (hundreds of
+        ctypes launches per step on the large configs, most of the step on
+        the small ones).  The zero-pivot flag is still read from `self.err`.
+        """
+        stream = torch.cuda.Stream(self.device)
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(stream):
+            if warmup:  # first calls create streams, set kernel attributes, size workspaces
+                self.factor(threshold, stream)
+                self.solve_into(b, x, stream)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            st = torch.cuda.current_stream(self.device)
+            self.factor(threshold, st)
+            self.solve_into(b, x, st)
+        torch.cuda.current_stream(self.device).wait_stream(stream)
+        return g
 
     def launches_per_factor(self) -> int:
         """Kernel launches one factorization issues (tf_level_launch_count)."""

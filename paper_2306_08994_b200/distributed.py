@@ -13,7 +13,7 @@ bitwise identical for any rank count.
 Data crosses ranks only where the tree does:
   factor / forward solve: a child's update block goes to its parent's owner;
   backward solve: a parent's solution block goes to the child's owner;
-  end of solve: the per-rank solution rows are summed (all-reduce).
+  end of solve: every rank's own solution rows are all-gathered.
 These are point-to-point transfers issued per level through a `Comm`:
 `TorchComm` (torch.distributed P2P, NCCL over NVLink on a GPU box; gloo on
 CPU) or `LocalComm` (all ranks simulated in one process on one device: the
@@ -160,6 +160,49 @@ class TorchComm:
     def broadcast(self, t, src: int):
         self.dist.broadcast(t, src, group=self.group)
 
+    def allgather(self, out_list, t):
+        self.dist.all_gather(out_list, t, group=self.group)
+
+
+class HostStagedComm(TorchComm):
+    """TorchComm over a CPU backend (gloo) for device tensors: every transfer
+    is staged through host memory.  Lets several processes share ONE GPU in
+    tests of the multi-process path (the ranks never wait on each other's
+    kernels: all waiting happens in gloo on the host)."""
+
+    def p2p(self, sends, recvs):
+        hs = [(t.detach().cpu(), d) for t, d in sends]
+        hr = [(torch_empty_like_cpu(t), s) for t, s in recvs]
+        super().p2p(hs, hr)
+        for (t, _), (h, _) in zip(recvs, hr):
+            t.copy_(h)
+
+    def allreduce_sum(self, t):
+        h = t.detach().cpu()
+        super().allreduce_sum(h)
+        t.copy_(h)
+
+    def allreduce_min(self, t):
+        h = t.detach().cpu()
+        super().allreduce_min(h)
+        t.copy_(h)
+
+    def broadcast(self, t, src: int):
+        h = t.detach().cpu()
+        super().broadcast(h, src)
+        t.copy_(h)
+
+    def allgather(self, out_list, t):
+        hs = [torch_empty_like_cpu(o) for o in out_list]
+        super().allgather(hs, t.detach().cpu())
+        for o, h in zip(out_list, hs):
+            o.copy_(h)
+
+
+def torch_empty_like_cpu(t):
+    import torch
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu")
+
     def allreduce_min(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
 
@@ -184,7 +227,7 @@ class RankState:
         import torch
         self.dp, self.shard, self.rank = dp, shard, rank
         dev = dp.device
-        self.views, self.fac, self.aux = [], [], []
+        self.views, self.fac, self.aux, self.ws = [], [], [], []
         upd_max = 1
         for L, dl in enumerate(dp.levels):
             f0, f1 = shard.levels[L].ranges[rank]
@@ -197,6 +240,8 @@ class RankState:
             if dl.aux_stride > 0:
                 aux = torch.empty(max(1, n * dl.aux_stride), dtype=torch.float64, device=dev)
                 v.aux = aux.data_ptr()
+            wsb = int(dp.lib.tf_level_factor_workspace(C.byref(v))) if n > 0 else 0
+            self.ws.append((torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None, wsb))
             self.views.append(v)
             self.fac.append(fac)
             self.aux.append(aux)
@@ -223,7 +268,8 @@ class RankState:
                                     C.c_void_p(dp.elem.data_ptr() + 8 * f0 * dl.view.elem_stride),
                                     C.c_void_p(self.fac[L].data_ptr()), C.c_void_p(out),
                                     C.c_double(threshold), C.c_void_p(self.err.data_ptr()),
-                                    None, 0, sp)
+                                    None if self.ws[L][0] is None else
+                                    C.c_void_p(self.ws[L][0].data_ptr()), self.ws[L][1], sp)
         _lib.check(rc, f"tf_level_factor(rank {self.rank}, level {L})")
 
 
@@ -348,6 +394,20 @@ class ShardedFactorization:
         dp = self.dp
         self._slots = {r: [self._solve_slots(r, L) for L in range(len(dp.levels))]
                        for r in self.ranks}
+        # pivot-order rows each rank owns (one contiguous range per level)
+        self._own = []
+        for r in range(self.world):
+            parts = []
+            for L, dl in enumerate(dp.levels):
+                f0, f1 = self.shard.levels[L].ranges[r]
+                if f1 > f0:
+                    lt = dl.tables
+                    a = int(lt.piv_off[f0])
+                    z = int(lt.piv_off[f1]) if f1 < lt.n_fronts else lt.piv_base + lt.n_pivots
+                    parts.append(np.arange(a, z, dtype=np.int64))
+            idx = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+            self._own.append(torch.from_numpy(idx).to(dp.device))
+        self._own_max = max(1, max(len(o) for o in self._own))
         self._blk, self._y, self._ws = {}, {}, {}
         for r in self.ranks:
             n = max((hi - lo) * dp.levels[L].max_m for L, (lo, hi) in enumerate(self._slots[r]))
@@ -437,23 +497,29 @@ class ShardedFactorization:
                     dp.levels[L].max_m, C.c_void_p(self._y[r].data_ptr()), nrhs,
                     C.c_void_p(ws.data_ptr()), wsb, sp)
                 _lib.check(rc, f"tf_level_solve_bwd(rank {r}, level {L})")
-        # keep each rank's own pivot rows, sum across ranks, scatter to natural order
-        for r in self.ranks:
-            keep = torch.zeros(dp.n_pivots, dtype=torch.bool, device=dp.device)
-            for L, dl in enumerate(dp.levels):
-                f0, f1 = self.shard.levels[L].ranges[r]
-                if f1 > f0:
-                    lt = dl.tables
-                    a = int(lt.piv_off[f0])
-                    z = int(lt.piv_off[f1]) if f1 < lt.n_fronts else lt.piv_base + lt.n_pivots
-                    keep[a:z] = True
-            yv = self._y[r][:dp.n_pivots * nrhs].view(dp.n_pivots, nrhs)
-            yv[~keep] = 0.0
-        ys = [self._y[r] for r in self.ranks]
+        # every rank's own pivot rows -> every rank (all-gather of owned rows,
+        # n x nrhs doubles received per rank), then scatter to natural order
+        npiv = dp.n_pivots
+
+        def rows(r):
+            return self._y[r][:npiv * nrhs].view(npiv, nrhs)
+
         if isinstance(self.comm, LocalComm):
-            self.comm.allreduce_sum(ys)
+            y0 = rows(self.ranks[0])
+            for r in self.ranks[1:]:
+                y0[self._own[r]] = rows(r)[self._own[r]]
+            ys = [self._y[self.ranks[0]]]
         else:
-            self.comm.allreduce_sum(ys[0])
+            me = self.ranks[0]
+            send = torch.zeros((self._own_max, nrhs), dtype=torch.float64, device=dp.device)
+            send[:len(self._own[me])] = rows(me)[self._own[me]]
+            outs = [torch.empty_like(send) for _ in range(self.world)]
+            self.comm.allgather(outs, send)
+            y0 = rows(me)
+            for r in range(self.world):
+                if r != me:
+                    y0[self._own[r]] = outs[r][:len(self._own[r])]
+            ys = [self._y[me]]
         if x.data_ptr() != b.data_ptr():
             x.copy_(b)
         _lib.check(lib.tf_permute_rows(po, dp.n_pivots, C.c_void_p(ys[0].data_ptr()),

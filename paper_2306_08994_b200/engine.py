@@ -40,16 +40,72 @@ class ExecState:
     debug: bool = False
     compiled: Optional[DevicePlan] = None
     factors: Optional["FactorResult"] = None
+    system: object = None
 
 
 def init_state(system, plan, debug: bool = False) -> ExecState:
-    """Zero-pivot threshold = 1e-14 * max|A_ij| (engine.py:67-75)."""
-    return ExecState(zero_threshold=ZERO_PIVOT_RELATIVE * float(system.peak), debug=debug)
+    """Zero-pivot threshold = 1e-14 * max|A_ij| (engine.py:67-75); the system seeds the values."""
+    return ExecState(zero_threshold=ZERO_PIVOT_RELATIVE * float(system.peak), debug=debug,
+                     system=system)
+
+
+def leaf_values(fronts, system) -> np.ndarray:
+    """Numeric leaf-front values that make the factorization start from `system`.
+
+    The reference seeds its state with the assembled entries
+    (init_state, engine.py:67-75).  An `ElementSystem` over the plan's own
+    leaf fronts IS the sum of their element matrices, so those are uploaded
+    as they are.  Any other `GlobalSystem` (a dict of lower-triangle entries,
+    e.g. the reference's 1D assembly or one edited with `add`) is split over
+    the leaves: each stored entry goes, whole, to the first leaf front that
+    holds both of its indices, so the extend-add sums reproduce every entry
+    exactly.  An entry no leaf front covers, or an ElementSystem over other
+    fronts, raises ContractViolationError instead of factorizing a different
+    matrix.
+    """
+    from .errors import ContractViolationError
+    from .fem import ElementSystem
+    from .tree import sort_fronts
+    if system is None:
+        return fronts.values
+    if isinstance(system, ElementSystem) and not system.modified:
+        fs = system.fronts
+        if fs is not fronts:
+            fs = sort_fronts(fs)
+        if fs is fronts or (fs.dofs.shape == fronts.dofs.shape and
+                            np.array_equal(fs.dofs, fronts.dofs) and
+                            fs.values.shape == fronts.values.shape and
+                            np.array_equal(fs.values, fronts.values)):
+            return fronts.values
+        raise ContractViolationError("the system's element matrices are not the plan's leaf fronts")
+    entries = system.entries
+    n = len(fronts)
+    width = fronts.values.shape[-1]
+    vals = np.zeros((n, width, width))
+    assigned = set()
+    for e in range(n):
+        d = [int(g) for g in fronts.dofs_of(e)]
+        for a, ga in enumerate(d):
+            for b, gb in enumerate(d):
+                if ga >= gb and (ga, gb) not in assigned:
+                    v = entries.get((ga, gb))
+                    if v is None:
+                        continue
+                    vals[e, a, b] = v
+                    vals[e, b, a] = v
+                    assigned.add((ga, gb))
+    if len(assigned) != len(entries):
+        missing = next(k for k in entries if k not in assigned)
+        raise ContractViolationError(f"system entry {missing} lies outside every leaf front")
+    return vals
 
 
 def compile_execution(plan, schedule=None, state: Optional[ExecState] = None) -> DevicePlan:
-    """Upload the level tables once; reusable across factorizations (engine.py:335-344)."""
-    dp = DevicePlan(plan, plan.tree.fronts)
+    """Upload the level tables and leaf values once; reusable across factorizations
+    (engine.py:335-344).  The leaf values come from the state's system (leaf_values)."""
+    plan = _plan_of(plan)
+    system = state.system if state is not None and state.system is not None else plan.system
+    dp = DevicePlan(plan, plan.tree.fronts, values=leaf_values(plan.tree.fronts, system))
     dp.fuse_bottom = FUSE_BOTTOM
     if state is not None:
         state.compiled = dp
@@ -235,9 +291,11 @@ def run_concurrent(schedule, plan, state: ExecState, workers: int = 1, debug: bo
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() != workers:
         raise ValueError(f"workers={workers} needs an initialised torch.distributed group of "
                          f"{workers} ranks (one per GPU)")
-    from .distributed import ShardedFactorization, TorchComm
+    from .distributed import HostStagedComm, ShardedFactorization, TorchComm
     dp = compiled or state.compiled or compile_execution(plan, None, state)
-    sf = ShardedFactorization(dp, workers, TorchComm(), ranks=[dist.get_rank()])
+    # NCCL moves device buffers directly; a CPU backend (gloo) stages them through the host
+    comm = HostStagedComm() if dist.get_backend() == "gloo" else TorchComm()
+    sf = ShardedFactorization(dp, workers, comm, ranks=[dist.get_rank()])
     pos = sf.factor(state.zero_threshold)
     if pos >= 0:
         front, pivot = plan.locate_pivot(pos)

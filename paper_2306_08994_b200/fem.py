@@ -471,6 +471,14 @@ class ElementSystem(GlobalSystem):
     @entries.setter
     def entries(self, value):
         self._entries = value
+        self.modified = True
+
+    modified = False  # True once entries were edited: they no longer equal the element sum
+
+    def add(self, i: int, j: int, value: float) -> None:
+        super().add(i, j, value)
+        self.modified = True
+        self._peak = None
 
     @property
     def peak(self) -> float:
@@ -481,7 +489,7 @@ class ElementSystem(GlobalSystem):
     def matvec(self, u: np.ndarray) -> np.ndarray:
         u = np.asarray(u, dtype=float)
         fs = self.fronts
-        if not fs.uniform_size:
+        if not fs.uniform_size or self.modified:
             return super().matvec(u)
         idx = fs.dofs.astype(np.int64) - 1  # (n_el, nloc)
         ue = u[idx]  # (n_el, nloc, ...)
