@@ -31,6 +31,9 @@ from . import _lib
 # slower than the per-level kernels on B200 (tools/fuse_sweep.sh), so it is off
 # unless a cap is set.
 FUSE_CAP_DEFAULT = 0
+# ... except on small trees, where every level is a few microseconds of work and
+# the per-launch cost dominates (cfg1: 1024 leaves)
+FUSE_AUTO_MAX_LEAVES = 16384
 
 
 def _tri(n):
@@ -170,7 +173,10 @@ class DevicePlan:
             return 0
         arr = (_lib.LevelView * len(self.levels))(*[dl.view for dl in self.levels])
         n = int(self.lib.tf_subtree_fusable(C.cast(arr, C.c_void_p), len(self.levels)))
-        cap = int(os.environ.get("TFB_FUSE_LEVELS", str(self.fuse_cap)))
+        cap = self.fuse_cap
+        if cap == 0 and self.levels and self.levels[0].n_fronts <= FUSE_AUTO_MAX_LEAVES:
+            cap = 10  # launch-bound trees: one subtree launch instead of one per level
+        cap = int(os.environ.get("TFB_FUSE_LEVELS", str(cap)))
         n = min(n, cap)
         return n if n >= 2 else 0
 

@@ -157,6 +157,9 @@ class TorchComm:
     def allreduce_sum(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
 
+    def allreduce_min(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+
     def broadcast(self, t, src: int):
         self.dist.broadcast(t, src, group=self.group)
 
@@ -202,9 +205,6 @@ class HostStagedComm(TorchComm):
 def torch_empty_like_cpu(t):
     import torch
     return torch.empty(t.shape, dtype=t.dtype, device="cpu")
-
-    def allreduce_min(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
 
 
 # ------------------------------------------------------ per-rank GPU state
@@ -394,7 +394,25 @@ class ShardedFactorization:
         dp = self.dp
         self._slots = {r: [self._solve_slots(r, L) for L in range(len(dp.levels))]
                        for r in self.ranks}
-        # pivot-order rows each rank owns (one contiguous range per level)
+        self._own = None
+        self._blk, self._y, self._ws = {}, {}, {}
+        for r in self.ranks:
+            n = max((hi - lo) * dp.levels[L].max_m for L, (lo, hi) in enumerate(self._slots[r]))
+            self._blk[r] = [torch.empty(max(1, n * nrhs), dtype=torch.float64, device=dp.device)
+                            for _ in range(2)]
+            self._y[r] = torch.empty(max(1, dp.n_pivots * nrhs), dtype=torch.float64,
+                                     device=dp.device)
+            ws = max(int(dp.lib.tf_level_solve_workspace(C.byref(self.state[r].views[L]), nrhs))
+                     for L in range(len(dp.levels)))
+            self._ws[r] = (torch.empty(max(1, ws // 8), dtype=torch.float64, device=dp.device), ws)
+        self._nrhs = nrhs
+
+    def _owned_rows(self):
+        """Pivot-order rows each rank owns (one contiguous range per level)."""
+        import torch
+        if self._own is not None:
+            return self._own
+        dp = self.dp
         self._own = []
         for r in range(self.world):
             parts = []
@@ -408,17 +426,7 @@ class ShardedFactorization:
             idx = np.concatenate(parts) if parts else np.zeros(0, np.int64)
             self._own.append(torch.from_numpy(idx).to(dp.device))
         self._own_max = max(1, max(len(o) for o in self._own))
-        self._blk, self._y, self._ws = {}, {}, {}
-        for r in self.ranks:
-            n = max((hi - lo) * dp.levels[L].max_m for L, (lo, hi) in enumerate(self._slots[r]))
-            self._blk[r] = [torch.empty(max(1, n * nrhs), dtype=torch.float64, device=dp.device)
-                            for _ in range(2)]
-            self._y[r] = torch.empty(max(1, dp.n_pivots * nrhs), dtype=torch.float64,
-                                     device=dp.device)
-            ws = max(int(dp.lib.tf_level_solve_workspace(C.byref(self.state[r].views[L]), nrhs))
-                     for L in range(len(dp.levels)))
-            self._ws[r] = (torch.empty(max(1, ws // 8), dtype=torch.float64, device=dp.device), ws)
-        self._nrhs = nrhs
+        return self._own
 
     def _blk_slot(self, r: int, L: int, f: int, nrhs: int):
         lo = self._slots[r][L][0]
@@ -500,6 +508,7 @@ class ShardedFactorization:
         # every rank's own pivot rows -> every rank (all-gather of owned rows,
         # n x nrhs doubles received per rank), then scatter to natural order
         npiv = dp.n_pivots
+        self._owned_rows()
 
         def rows(r):
             return self._y[r][:npiv * nrhs].view(npiv, nrhs)

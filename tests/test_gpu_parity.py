@@ -38,8 +38,11 @@ def front_path(request, cuda_ok):
     from paper_2306_08994_b200 import device
     old = device.set_small_front_limit(1 if request.param == "large" else 232)
     device.FUSE_CAP_DEFAULT = 10 if request.param == "fused" else 0
+    auto = device.FUSE_AUTO_MAX_LEAVES
+    device.FUSE_AUTO_MAX_LEAVES = 0  # per-level kernels unless "fused"
     yield request.param
     device.FUSE_CAP_DEFAULT = 0
+    device.FUSE_AUTO_MAX_LEAVES = auto
     device.set_small_front_limit(old)
 
 
