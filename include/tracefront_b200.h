@@ -250,6 +250,12 @@ const char* tf_timing_class_name(int32_t cls);
 /* Library build identification (arch, compile flags). */
 const char* tf_build_info(void);
 
+/* Test hook (race detection without compute-sanitizer): seed != 0 makes the
+ * CTAs of the flag-synchronised kernels (root dataflow, wavefront sweeps)
+ * sleep pseudo-random times at each work item and after each acquire; 0
+ * restores normal scheduling.  Results must be bitwise unchanged. */
+int tf_set_jitter(uint32_t seed);
+
 #ifdef __cplusplus
 }
 #endif

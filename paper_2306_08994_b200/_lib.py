@@ -71,7 +71,7 @@ EXPORTS = (
     "tf_mesh_tensor", "tf_plan_create", "tf_plan_destroy", "tf_plan_summary_get",
     "tf_plan_level", "tf_plan_pivot_order", "tf_plan_node_lists", "tf_plan_node_lists_len",
     "tf_level_factor_workspace", "tf_level_factor", "tf_level_solve_fwd",
-    "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m",
+    "tf_level_solve_bwd", "tf_permute_rows", "tf_level_launch_count", "tf_set_small_max_m", "tf_set_jitter",
     "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_subtree_fusable",
     "tf_subtree_factor", "tf_timing_enable", "tf_timing_collect", "tf_timing_class_name",
     "tf_build_info", "tf_atomic_fnf",
@@ -130,6 +130,8 @@ def load() -> C.CDLL:
     lib.tf_permute_rows.restype = C.c_int
     lib.tf_level_launch_count.argtypes = [C.POINTER(LevelView), i32, i32]
     lib.tf_level_launch_count.restype = i32
+    lib.tf_set_jitter.argtypes = [C.c_uint32]
+    lib.tf_set_jitter.restype = C.c_int
     lib.tf_set_small_max_m.argtypes = [i32]
     lib.tf_set_small_max_m.restype = i32
     lib.tf_subtree_fusable.argtypes = [vp, i32]

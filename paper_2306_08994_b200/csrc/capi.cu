@@ -28,6 +28,8 @@ cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* 
                                   unsigned long long* err, cudaStream_t st);
 int large_level_launches(int max_k, int max_upd, long long level_fronts);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
+cudaError_t set_jitter_solve(unsigned seed);
+cudaError_t set_jitter_factor(unsigned seed);
 int g_small_max_m = 112;  // measured best split on B200 (tools/sweep.sh)
 }  // namespace tfb
 
@@ -156,4 +158,10 @@ extern "C" int32_t tf_set_small_max_m(int32_t m) {
 extern "C" const char* tf_build_info(void) {
   return "tfb200 sm_100a fp64 (DMMA m8n8k4 via mma.sync; cp.async staging); "
          "shared-memory fronts <= 232, blocked large fronts";
+}
+
+extern "C" int tf_set_jitter(uint32_t seed) {
+  cudaError_t e = set_jitter_factor(seed);
+  if (e == cudaSuccess) e = set_jitter_solve(seed);
+  return status(e);
 }

@@ -202,6 +202,25 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Scheduling perturbation for race tests (tf_set_jitter): when the seed is
+// non-zero, CTAs of the flag-synchronised kernels sleep a pseudo-random time
+// at the start of each work item and after each acquire, so producers and
+// consumers interleave differently run to run.  A missing wait or an early
+// publish then shows up as a result that differs from the unperturbed run.
+// One copy per translation unit (set through tf_set_jitter for all of them).
+static __device__ unsigned g_jitter_seed;
+__device__ __forceinline__ void tfb_jitter(unsigned salt) {
+  const unsigned seed = *(volatile unsigned*)&g_jitter_seed;
+  if (seed == 0) return;
+  unsigned h = (blockIdx.x * 0x9E3779B1u) ^ (salt * 0x85EBCA77u) ^ seed;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+  const unsigned ns = h & 0x3FFF;  // up to ~16 us
+  for (unsigned t = 0; t < ns; t += 1000) __nanosleep(1000);
+}
+inline cudaError_t set_jitter_tu(unsigned seed) {
+  return cudaMemcpyToSymbol(g_jitter_seed, &seed, sizeof(seed));
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -1020,6 +1020,7 @@ static_assert(GRoot::smem <= kRootSmem, "GEMM staging fits the tile buffers");
 
 __device__ __forceinline__ void root_wait(const int* flag) {
   while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+  tfb_jitter((unsigned)(size_t)flag);
 }
 __device__ __forceinline__ void root_publish(int* flag) {  // after a CTA barrier
   if (threadIdx.x == 0) {
@@ -1272,6 +1273,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
     __syncthreads();
     const long long t = s_tile;
     if (t >= ntiles) return;
+    if (tid == 0) tfb_jitter((unsigned)t);
     const long long f = t % nf;
     long long rr = t / nf;
     int l = 0;
@@ -1558,5 +1560,7 @@ int large_level_launches(int max_k, int max_upd, long long level_fronts) {
   return 1 + large_panel_launches(max_k, fronts) + (max_k > 0 && max_upd > 0 ? 1 : 0) +
          (max_k > 0 ? 1 : 0);
 }
+
+cudaError_t set_jitter_factor(unsigned seed) { return set_jitter_tu(seed); }
 
 }  // namespace tfb

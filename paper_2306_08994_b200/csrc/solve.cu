@@ -322,8 +322,10 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void wave_wait(const int* flag) {
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
     while (ld_acquire(flag) == 0) __nanosleep(20);
+    tfb_jitter((unsigned)(size_t)flag);
+  }
   __syncthreads();
 }
 __device__ __forceinline__ void wave_publish(int* flag) {
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(256)
   TFB_DIV_SETUP(nr);
   const long long nf = L.n_fronts, ntiles = (long long)rt_max * nf;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) tfb_jitter((unsigned)tile);
     const int R = (int)(tile / nf);
     const long long f = tile - (long long)R * nf;
     const Shape s = front_shape(L, f);
@@ -629,6 +632,7 @@ __global__ void __launch_bounds__(256)
     const long long npart = nf * (long long)max(0, rt_max - b - 2), count = npart + nf;
     for (; next < base + count; next += gridDim.x) {
       const long long item = next - base;
+      if (threadIdx.x == 0) tfb_jitter((unsigned)next);
       const bool partial = item < npart;
       const long long f = partial ? item % nf : item - npart;
       const int R = partial ? b + 2 + (int)(item / nf) : b + 1;
@@ -1852,5 +1856,7 @@ cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, d
   timer_end(st);
   return cudaGetLastError();
 }
+
+cudaError_t set_jitter_solve(unsigned seed) { return set_jitter_tu(seed); }
 
 }  // namespace tfb

@@ -40,6 +40,59 @@ def _tri(n):
     return n * (n + 1) // 2
 
 
+# Guard mode (tests; race/out-of-bounds detection without compute-sanitizer):
+# every kernel-written buffer gets GUARD_DOUBLES canary words on both sides,
+# and its interior is filled with a NaN before each factorization / solve, so
+# a stray write shows up in check_guards() and a read of unwritten data turns
+# the result into NaN.  Off by default (TFB_GUARD=1 or device.GUARD = True).
+GUARD = os.environ.get("TFB_GUARD", "0") == "1"
+GUARD_DOUBLES = 4096
+_CANARY = -0x0123456789ABCDF  # int64 bit pattern of the guard words (a NaN-free double)
+_guarded: list = []
+
+
+def _buf(n: int, device, dtype=torch.float64) -> torch.Tensor:
+    """Device buffer of n elements (guard bands around it in guard mode)."""
+    n = max(1, int(n))
+    if not GUARD:
+        return torch.empty(n, dtype=dtype, device=device)
+    per = 8 // torch.empty(0, dtype=dtype).element_size()
+    g = GUARD_DOUBLES * per
+    big = torch.empty(n + 2 * g, dtype=dtype, device=device)
+    words = big.view(torch.int64) if dtype != torch.uint8 else None
+    if words is None:  # byte buffers: whole words of guard on each side
+        big.view(torch.uint8).fill_(0xA5)
+    else:
+        words.fill_(_CANARY)
+    inner = big[g:g + n]
+    inner.fill_(float("nan") if dtype == torch.float64 else 0)
+    _guarded.append((big, g, n, dtype))
+    return inner
+
+
+def check_guards() -> list:
+    """Indices of guarded buffers whose canaries were overwritten (guard mode)."""
+    bad = []
+    for i, (big, g, n, dtype) in enumerate(_guarded):
+        if dtype == torch.uint8:
+            ok = bool((big[:g] == 0xA5).all() and (big[g + n:] == 0xA5).all())
+        else:
+            w = big.view(torch.int64)
+            per = big.element_size() // 8 or 1
+            ok = bool((w[:g // per] == _CANARY).all() and (w[(g + n) // per:] == _CANARY).all())
+        if not ok:
+            bad.append(i)
+    return bad
+
+
+def poison(*tensors) -> None:
+    """Guard mode: fill kernel outputs with NaN so stale reads propagate."""
+    if GUARD:
+        for t in tensors:
+            if t is not None and t.dtype == torch.float64:
+                t.fill_(float("nan"))
+
+
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2306_08994_b200 needs a CUDA device (sm_100a); "
@@ -97,16 +150,14 @@ class DeviceLevel:
         self.aux_stride = int(lib.tf_level_aux_doubles(C.byref(v)))
         self.aux = None
         if self.aux_stride > 0:
-            self.aux = torch.empty(self.n_fronts * self.aux_stride, dtype=torch.float64,
-                                   device=device)
+            self.aux = _buf(self.n_fronts * self.aux_stride, device)
             v.aux = self.aux.data_ptr()
             v.aux_stride = self.aux_stride
         self.view = v
         # factor scratch owned by this plan (root-dataflow flags): concurrent
         # factorizations of different plans never share it
         self.ws_bytes = int(lib.tf_level_factor_workspace(C.byref(v)))
-        self.ws = (torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
-                   if self.ws_bytes > 0 else None)
+        self.ws = _buf(self.ws_bytes, device, torch.uint8) if self.ws_bytes > 0 else None
 
     @property
     def large(self) -> bool:
@@ -143,8 +194,7 @@ class DevicePlan:
     @property
     def factors(self):
         if self._factors is None:
-            self._factors = [torch.empty(max(1, dl.n_fronts * dl.fac_stride),
-                                         dtype=torch.float64, device=self.device)
+            self._factors = [_buf(dl.n_fronts * dl.fac_stride, self.device)
                              for dl in self.levels]
         return self._factors
 
@@ -152,8 +202,7 @@ class DevicePlan:
     def upd(self):
         if self._upd is None:
             upd_max = max(dl.n_fronts * dl.upd_stride for dl in self.levels)
-            self._upd = [torch.empty(max(1, upd_max), dtype=torch.float64, device=self.device)
-                         for _ in range(2)]
+            self._upd = [_buf(upd_max, self.device) for _ in range(2)]
         return self._upd
 
     # ---- factorization -----------------------------------------------------------
@@ -189,6 +238,8 @@ class DevicePlan:
         st = stream or torch.cuda.current_stream(self.device)
         sp = C.c_void_p(st.cuda_stream)
         self.err.fill_(-1)
+        if GUARD:
+            poison(*self.factors, *self.upd, *[dl.aux for dl in self.levels])
         nf = self.fused_levels
         if nf >= 2:
             views = (_lib.LevelView * nf)(*[dl.view for dl in self.levels[:nf]])
@@ -214,13 +265,11 @@ class DevicePlan:
     def _blocks(self, nrhs: int):
         if self._solve_nrhs != nrhs:
             n = max(dl.n_fronts * dl.max_m for dl in self.levels) * nrhs
-            self._blk = [torch.empty(max(1, n), dtype=torch.float64, device=self.device)
-                         for _ in range(2)]
-            self._y = torch.empty(max(1, self.n_pivots * nrhs), dtype=torch.float64,
-                                  device=self.device)
+            self._blk = [_buf(n, self.device) for _ in range(2)]
+            self._y = _buf(self.n_pivots * nrhs, self.device)
             ws = max(int(self.lib.tf_level_solve_workspace(C.byref(dl.view), nrhs))
                      for dl in self.levels)
-            self._ws = torch.empty(max(1, ws // 8), dtype=torch.float64, device=self.device)
+            self._ws = _buf(ws // 8, self.device)
             self._ws_bytes = ws
             self._solve_nrhs = nrhs
         return self._blk
@@ -234,6 +283,8 @@ class DevicePlan:
         lib = self.lib
         blk = self._blocks(nrhs)
         y = self._y
+        if GUARD:
+            poison(*blk, y)  # (the workspace's flags must start at zero: not poisoned)
         npiv = self.n_pivots
         if x.data_ptr() != b.data_ptr():
             x.copy_(b)  # DOFs outside every front stay as given (engine.py:481)
