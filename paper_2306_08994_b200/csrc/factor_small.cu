@@ -59,12 +59,18 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
                                              const double* __restrict__ src1, double* F,
                                              double* lv, double* __restrict__ fac_out,
                                              double* __restrict__ upd_dst, double threshold,
-                                             unsigned long long* err, int t, int bar) {
+                                             unsigned long long* err, int t, int bar,
+                                             int fs_k = 16) {
   const int m = S.m, k = S.k, kp = S.kp, u = m - k;
   const int ks = kp + 1, tk = (int)tri32(k, 0), nS = (int)tri32(u, 0), s0 = tk + u * ks;
   double* Sb = F + s0;
   auto rowp = [&](int r) { return r < k ? (int)tri32(r, 0) : tk + (r - k) * ks; };
-  for (int e = t; e < s0 + nS; e += G) F[e] = 0.0;
+  {  // zero the front: 16-byte stores (F is 16-byte aligned), odd tail scalar
+    const int n2 = (s0 + nS) >> 1;
+    double2* F2 = reinterpret_cast<double2*>(F);
+    for (int e = t; e < n2; e += G) F2[e] = make_double2(0.0, 0.0);
+    if (t == 0 && ((s0 + nS) & 1)) F[s0 + nS - 1] = 0.0;
+  }
   group_sync<G>(bar);
 
   // (1) extend-add through the scatter table: sources in fixed order, no atomics
@@ -97,18 +103,30 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
 #pragma unroll
         for (int q = 0; q < 4; q++) F[p[q]] += v[q];
       }
-      for (; e < n; e += G) F[__ldg(scc + e)] += src[e];
+      if (e < n) {  // remainder: up to four entries per thread, loads first
+        int p[4];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const bool ok = e + q * G < n;
+          p[q] = ok ? __ldg(scc + e + q * G) : -1;
+          v[q] = ok ? src[e + q * G] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (p[q] >= 0) F[p[q]] += v[q];
+      }
     }
     group_sync<G>(bar);
   }
 
-  // (2) panel.  Wide groups (G >= 128, the larger fronts) with k >= 16:
+  // (2) panel.  Wide groups (G >= 32) with k >= fs_k (TFB_SMALL_FSK, measured):
   // (a) the k x k pivot block, right-looking with unscaled columns (one
   // barrier per pivot), scaled to l; (b) every L21 row independently (no
   // barriers): forward substitution against L11, u_rc = a_rc - sum_{q<c}
   // u_rq l(c,q), then l(r,c) = u_rc / d_c.
-  if constexpr (G >= 128) {
-    if (k >= 16) {
+  if constexpr (G >= 32) {
+    if (k >= fs_k) {
       const long long piv0 = L.piv_off[f];
       for (int c = 0; c < k; c++) {
         const double d = F[tri32(c, c)];
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(G* GPC)
     factor_small_kernel(LevelArgs L, const double* __restrict__ child_upd,
                         const double* __restrict__ elem, double* __restrict__ factors,
                         double* __restrict__ upd_out, double threshold,
-                        unsigned long long* err, int smem_per_group) {
+                        unsigned long long* err, int smem_per_group, int fs_k) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gid = threadIdx.x / G;
   const int t = threadIdx.x - gid * G;
@@ -254,7 +272,7 @@ __global__ void __launch_bounds__(G* GPC)
                                : child_upd + L.child_slot(f, 0) * L.child_upd_stride;
   const double* s1 = L.is_leaf ? nullptr : child_upd + L.child_slot(f, 1) * L.child_upd_stride;
   factor_front<G>(L, f, S, s0, s1, F, lv, factors + f * L.fac_stride,
-                  upd_out + f * L.upd_stride, threshold, err, t, 1 + gid);
+                  upd_out + f * L.upd_stride, threshold, err, t, 1 + gid, fs_k);
 }
 
 template <int G, int GPC>
@@ -272,8 +290,13 @@ static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, c
   }
   const long long blocks = (L.n_fronts + GPC - 1) / GPC;
   timer_begin(K_SMALL, st);
+  static int fs_k = -1;
+  if (fs_k < 0) {
+    const char* e = getenv("TFB_SMALL_FSK");
+    fs_k = e ? atoi(e) : 16;
+  }
   kern<<<(unsigned)blocks, G * GPC, smem, st>>>(L, child_upd, elem, factors, upd_out, thr, err,
-                                                per);
+                                                per, fs_k);
   timer_end(st);
   return cudaGetLastError();
 }

@@ -54,7 +54,9 @@ assert np.abs(base_x[:, 0] - xr).max() / np.abs(xr).max() <= 1e-10
 for seed in (1, 2, 3):
     assert lib.tf_set_jitter(seed) == 0
     f2, x2 = run()
-    assert all(torch.equal(a, b) for a, b in zip(base_f, f2)), f"factors differ under jitter {{seed}}"
+    # bit patterns (slots no kernel writes stay NaN-poisoned in both runs)
+    assert all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(base_f, f2)), \
+        f"factors differ under jitter {{seed}}"
     assert np.array_equal(x2, base_x), f"solution differs under jitter {{seed}}"
     assert device.check_guards() == []
 lib.tf_set_jitter(0)
