@@ -159,6 +159,9 @@ typedef struct {
   int64_t child_base; /* tree index of the front held in slot 0 of the child-level buffer */
   int64_t level_fronts; /* fronts of the whole level (a slice keeps the full count, so every
                            rank picks the same kernel variants) */
+  const uint8_t* zero_upd; /* optional, per front: 1 when the front and its whole subtree have
+                              no pivots, so its forward update block is identically zero: the
+                              solve neither writes nor reads it (NULL: leaves with k == 0 only) */
 } tf_level_view;
 
 /* Doubles of `aux` each front of this level needs under the current

@@ -62,7 +62,7 @@ class LevelView(C.Structure):
         ("pat", C.c_void_p), ("maps", C.c_void_p),
         ("aux", C.c_void_p), ("aux_stride", C.c_int64),
         ("front_base", C.c_int64), ("child_base", C.c_int64),
-        ("level_fronts", C.c_int64),
+        ("level_fronts", C.c_int64), ("zero_upd", C.c_void_p),
     ]
 
 

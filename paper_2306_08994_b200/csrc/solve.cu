@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(G* GPC)
   double* W = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  if (L.is_leaf && k == 0) return;  // element without pivots: zero update, not written (parent skips it)
+  if (L.upd_is_zero(f)) return;  // pivot-free subtree: zero update, not written (parent skips it)
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(G* GPC)
     for (int c = 0; c < s.nsrc; c++) {
       const long long ch = 2 * (L.front_base + f) + c - C.front_base;
       const int ck = C.pat[(size_t)C.pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
-      if (C.is_leaf && ck == 0) continue;  // element without pivots: zero update, never written
+      if (C.upd_is_zero(ch)) continue;  // pivot-free child subtree: zero update, never written
       const int off = child_at0 ? 0 : ck;
       const int len = c == 0 ? s.len0 : s.len1;
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(G* GPC)
   double* X = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  if (L.is_leaf && k == 0) return;  // nothing to solve and no children to serve
+  if (L.upd_is_zero(f)) return;  // pivot-free subtree: nothing to solve, no children to serve
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -1661,7 +1661,7 @@ static unsigned wave_grid(K kern, size_t smem, long long ntiles) {
 __global__ void __launch_bounds__(256)
     zero_unpivoted_leaf_blocks(LevelArgs C, double* w, long long per_front) {
   for (long long f = blockIdx.x; f < C.n_fronts; f += gridDim.x) {
-    if (C.pat[(size_t)C.pattern_of[f] * TF_PAT_WIDTH + TF_PAT_K] != 0) continue;
+    if (!C.upd_is_zero(f)) continue;
     for (long long i = threadIdx.x; i < per_front; i += blockDim.x) w[f * per_front + i] = 0.0;
   }
 }
@@ -1674,7 +1674,7 @@ cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const doubl
   // Leaf elements without pivots never write their (zero) update blocks; the
   // group kernels skip such children, every other kernel gets them zeroed.
   const bool small = !level_is_large(L.is_leaf, L.max_m);
-  if (C.is_leaf && w_child && C.n_fronts > 0 && (!small || warp16_solve(L, nrhs))) {
+  if ((C.is_leaf || C.zero_upd) && w_child && C.n_fronts > 0 && (!small || warp16_solve(L, nrhs))) {
     zero_unpivoted_leaf_blocks<<<(unsigned)std::min<long long>(C.n_fronts, 148 * 8), 256, 0, st>>>(
         C, const_cast<double*>(w_child), child_rows * nrhs);
     cudaError_t e = cudaGetLastError();

@@ -178,8 +178,23 @@ class DevicePlan:
         self.elem = torch.from_numpy(vals.ravel()).to(self.device)
         self.levels: list[DeviceLevel] = []
         child = 0
+        zprev = None
         for lt in native.levels:
             dl = DeviceLevel(self.lib, lt, self.device, child, elem_stride, elem_ld)
+            # pivot-free subtrees: the front has no pivots and neither has any
+            # descendant, so its forward update block is zero (the solve skips it)
+            z = lt.front_k() == 0
+            if zprev is not None:
+                kids = np.ones(lt.n_fronts, dtype=bool)
+                nc = len(zprev)
+                i = np.arange(lt.n_fronts)
+                kids &= zprev[np.minimum(2 * i, nc - 1)]
+                has2 = 2 * i + 1 < nc
+                kids[has2] &= zprev[2 * i[has2] + 1]
+                z &= kids
+            dl.zero_upd = torch.from_numpy(z.astype(np.uint8)).to(self.device)
+            dl.view.zero_upd = dl.zero_upd.data_ptr()
+            zprev = z
             self.levels.append(dl)
             child = dl.upd_stride
         self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)

@@ -217,6 +217,8 @@ def _slice_view(full, f0: int, n: int, child_base: int = 0):
     v.piv_off = (full.piv_off or 0) + 8 * f0
     v.front_base = f0
     v.child_base = child_base
+    if full.zero_upd:
+        v.zero_upd = full.zero_upd + f0
     return v
 
 
