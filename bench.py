@@ -171,6 +171,37 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------ scaling model
+NVLINK_GBS = 450.0  # effective one-direction NVLink 5 P2P bandwidth assumed per transfer
+
+
+def modelled_scaling(dp, level_ms, solve_ms, worlds=(2, 4, 8)):
+    """Strong-scaling model of the subtree-sharded path from
+    the MEASURED one-GPU per-level times: a level with n_L fronts on P GPUs takes
+    level_ms x (most fronts any rank owns) / n_L (independent fronts split
+    evenly; the top log2 P levels keep whole fronts on single GPUs), plus the
+    root-ward packed Schur complements of every cross-rank tree edge at
+    NVLINK_GBS.  The solve scales like the factorization's level profile.  A
+    model, not a measurement: this pool has one GPU per box."""
+    from paper_2306_08994_b200.distributed import ShardPlan
+    sizes = [dl.n_fronts for dl in dp.levels]
+    t1 = float(sum(level_ms)) + solve_ms
+    out = {}
+    for P in worlds:
+        sp = ShardPlan(sizes, P)
+        t = 0.0
+        for L, ls in enumerate(sp.levels):
+            most = max(f1 - f0 for f0, f1 in ls.ranges)
+            t += level_ms[L] * most / max(sizes[L], 1)
+            if L > 0:
+                for c, q, p_ in sp.upward(L):
+                    t += 8.0 * dp.levels[L - 1].upd_stride / (NVLINK_GBS * 1e6)
+        ts = solve_ms * (t / max(sum(level_ms), 1e-9))
+        out[str(P)] = {"ms_per_step": t + ts, "speedup": t1 / (t + ts),
+                       "efficiency": t1 / (P * (t + ts)), "split_level": sp.split}
+    return out
+
+
 # ---------------------------------------------------------------------- ours
 def run_ours(args, cfg):
     import torch
@@ -406,6 +437,8 @@ def run_ours(args, cfg):
         "clocks": clk.summary(),
         "roofline": roof,
         "level_ms": [round(float(t), 4) for t in level_ms],
+        "modelled_scaling": (modelled_scaling(dp, level_ms, eager_ms - float(level_ms.sum()))
+                             if world == 1 else None),
         "kernel_ms_per_step": kernel_ms,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
