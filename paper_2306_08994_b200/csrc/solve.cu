@@ -282,6 +282,278 @@ __global__ void __launch_bounds__(G* GPC)
   }
 }
 
+// Many right-hand sides on small levels: one warp per front, lane l owns
+// columns col0 + l + 32j (j < CPL), and the front is processed in the GATHER
+// form, so no vector block is materialised:
+//   pivot rows  w_c = y_c + sum_children child[inv(c)]      (registers, c < k)
+//               w_r -= l(r,c) w_c  for c < r < k            (forward elimination)
+//               y_c = w_c / d_c
+//   update rows u_{r-k} = sum_children child[inv(r)] - sum_c l(r,c) w_c   (streamed)
+// Child rows come through the inverse extend-add maps (front row -> child
+// update row); pivot-free child subtrees are skipped.  No shared memory, no
+// index division, every vector access a coalesced 32*8-byte row segment;
+// the update rows are streamed four at a time (all their loads in flight).
+constexpr int kColsWarps = 8;
+template <int KMAX, int CPL>
+__global__ void __launch_bounds__(32 * kColsWarps)
+    solve_fwd_cols(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
+                   const double* __restrict__ w_child, long long child_rows, int child_at0,
+                   double* __restrict__ w_out, long long out_rows, double* __restrict__ y, int nr,
+                   int ldr, int col0) {
+  const int lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kColsWarps + (threadIdx.x >> 5);
+  if (f >= L.n_fronts || L.upd_is_zero(f)) return;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pg = factors + f * L.fac_stride;
+  const int* inv0 = L.maps + s.ioff;
+  const int* inv1 = inv0 + m;
+  // child blocks (null: no such child or a pivot-free subtree)
+  const double* Wc0 = nullptr;
+  const double* Wc1 = nullptr;
+  if (!L.is_leaf) {
+    const long long ch0 = 2 * (L.front_base + f) - C.front_base;
+    if (!C.upd_is_zero(ch0)) {
+      const int ck = C.pat[(size_t)C.pattern_of[ch0] * TF_PAT_WIDTH + TF_PAT_K];
+      Wc0 = w_child + (ch0 * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+    }
+    if (s.nsrc == 2 && !C.upd_is_zero(ch0 + 1)) {
+      const int ck = C.pat[(size_t)C.pattern_of[ch0 + 1] * TF_PAT_WIDTH + TF_PAT_K];
+      Wc1 = w_child + ((ch0 + 1) * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+    }
+  }
+  bool cok[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; j++) cok[j] = lane + 32 * j < nr;
+  auto child_sum = [&](int r, double (&v)[CPL]) {
+    const int i0 = Wc0 ? __ldg(inv0 + r) : -1;
+    const int i1 = Wc1 ? __ldg(inv1 + r) : -1;
+#pragma unroll
+    for (int j = 0; j < CPL; j++) {
+      const int col = lane + 32 * j;
+      double a = (i0 >= 0 && cok[j]) ? Wc0[(long long)i0 * ldr + col] : 0.0;
+      double b = (i1 >= 0 && cok[j]) ? Wc1[(long long)i1 * ldr + col] : 0.0;
+      v[j] = a + b;
+    }
+  };
+  // pivot rows
+  double w[KMAX][CPL];
+#pragma unroll
+  for (int c = 0; c < KMAX; c++) {
+    if (c < k) {
+      double v[CPL];
+      child_sum(c, v);
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        w[c][j] = v[j] + (cok[j] ? y[(piv + c) * ldr + col0 + lane + 32 * j] : 0.0);
+    } else {
+#pragma unroll
+      for (int j = 0; j < CPL; j++) w[c][j] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KMAX; c++) {
+#pragma unroll
+    for (int r = c + 1; r < KMAX; r++) {
+      if (r < k) {
+        const double lrc = __ldg(Pg + (long long)r * kp + c);
+#pragma unroll
+        for (int j = 0; j < CPL; j++) w[r][j] -= lrc * w[c][j];
+      }
+    }
+  }
+  const double* dv = Pg + (long long)m * kp;
+#pragma unroll
+  for (int c = 0; c < KMAX; c++) {
+    if (c < k) {
+      const double dinv = 1.0 / __ldg(dv + c);
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        if (cok[j]) y[(piv + c) * ldr + col0 + lane + 32 * j] = w[c][j] * dinv;
+    }
+  }
+  // update rows, four at a time
+  double* out = w_out + f * out_rows * ldr + col0;
+  for (int r0 = k; r0 < m; r0 += 4) {
+    double v[4][CPL];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      if (r0 + q < m) child_sum(r0 + q, v[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int r = r0 + q;
+      if (r < m) {
+      const double* lr = Pg + (long long)r * kp;
+#pragma unroll
+      for (int c = 0; c < KMAX; c++) {
+        if (c < k) {
+          const double l = __ldg(lr + c);
+#pragma unroll
+          for (int j = 0; j < CPL; j++) v[q][j] -= l * w[c][j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        if (cok[j]) out[(long long)(r - k) * ldr + lane + 32 * j] = v[q][j];
+      }
+    }
+  }
+}
+
+// Backward counterpart, same layout (warp per front, lanes own columns):
+//   x_r (r >= k) = parent block rows gathered through the parent's map
+//   x_c = y_c - sum_{r>=k} l(r,c) x_r      (streamed over r, four rows at a time)
+//   x_c -= l(c',c) x_c' for c' > c        (back substitution in registers)
+//   y_c = x_c; the full block (m rows) goes to x_out for the children.
+template <int KMAX, int CPL>
+__global__ void __launch_bounds__(32 * kColsWarps)
+    solve_bwd_cols(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
+                   const double* __restrict__ x_parent, long long parent_rows,
+                   double* __restrict__ x_out, long long out_rows, double* __restrict__ y, int nr,
+                   int ldr, int col0) {
+  const int lane = threadIdx.x & 31;
+  const long long f = (long long)blockIdx.x * kColsWarps + (threadIdx.x >> 5);
+  if (f >= L.n_fronts || L.upd_is_zero(f)) return;
+  const Shape s = front_shape(L, f);
+  const int m = s.m, k = s.k, kp = s.kp;
+  const long long piv = L.piv_off[f];
+  const double* Pg = factors + f * L.fac_stride;
+  bool cok[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; j++) cok[j] = lane + 32 * j < nr;
+  const int* mp = nullptr;
+  const double* Xp = nullptr;
+  if (has_parent && m > k) {
+    const long long pf = ((L.front_base + f) >> 1) - PA.front_base;
+    const int c = (int)((L.front_base + f) & 1);
+    const int* PP = PA.pat + (size_t)PA.pattern_of[pf] * TF_PAT_WIDTH;
+    mp = PA.maps + (c == 0 ? PP[TF_PAT_OFF0] : PP[TF_PAT_OFF1]);
+    Xp = x_parent + pf * parent_rows * ldr + col0;
+  }
+  double x[KMAX][CPL];
+#pragma unroll
+  for (int c = 0; c < KMAX; c++)
+#pragma unroll
+    for (int j = 0; j < CPL; j++)
+      x[c][j] = (c < k && cok[j]) ? y[(piv + c) * ldr + col0 + lane + 32 * j] : 0.0;
+  double* out = L.is_leaf ? nullptr : x_out + f * out_rows * ldr + col0;
+  if (mp) {
+    for (int r0 = k; r0 < m; r0 += 4) {
+      double v[4][CPL];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        if (r0 + q < m) {
+          const long long pr = __ldg(mp + (r0 + q - k));
+#pragma unroll
+          for (int j = 0; j < CPL; j++) v[q][j] = cok[j] ? Xp[pr * ldr + lane + 32 * j] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int r = r0 + q;
+        if (r < m) {
+          const double* lr = Pg + (long long)r * kp;
+#pragma unroll
+          for (int c = 0; c < KMAX; c++) {
+            if (c < k) {
+              const double l = __ldg(lr + c);
+#pragma unroll
+              for (int j = 0; j < CPL; j++) x[c][j] -= l * v[q][j];
+            }
+          }
+          if (out) {
+#pragma unroll
+            for (int j = 0; j < CPL; j++)
+              if (cok[j]) out[(long long)r * ldr + lane + 32 * j] = v[q][j];
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = KMAX - 1; c > 0; c--) {
+    if (c < k) {
+#pragma unroll
+      for (int r = 0; r < c; r++) {
+        const double l = __ldg(Pg + (long long)c * kp + r);
+#pragma unroll
+        for (int j = 0; j < CPL; j++) x[r][j] -= l * x[c][j];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KMAX; c++) {
+    if (c < k) {
+#pragma unroll
+      for (int j = 0; j < CPL; j++) {
+        if (!cok[j]) continue;
+        y[(piv + c) * ldr + col0 + lane + 32 * j] = x[c][j];
+        if (out) out[(long long)c * ldr + lane + 32 * j] = x[c][j];
+      }
+    }
+  }
+}
+
+// Selection: many columns on small levels with few pivots per front
+// (TFB_COLS_SOLVE=0 disables, for A/B).
+static bool cols_solve_fwd(const LevelArgs& L, int nrhs) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_COLS_SOLVE");
+    v = e ? atoi(e) : 1;
+  }
+  // measured on cfg3 (64 RHS): faster for fronts of 12..27 rows with <= 4
+  // pivots (L3-L5: 1.37 -> 0.94 ms fwd+bwd), slower for tiny fronts (L2) and
+  // for k = 8..16 (L6-L9: register-resident pivot rows too long)
+  return v != 0 && nrhs >= 16 && L.max_k <= 4 && L.max_m >= 12 &&
+         !level_is_large(L.is_leaf, L.max_m);
+}
+
+static cudaError_t launch_bwd_cols(const LevelArgs& L, const LevelArgs& PA, int has_parent,
+                                   const double* factors, const double* x_parent,
+                                   long long parent_rows, double* x_out, long long out_rows,
+                                   double* y, int nrhs, cudaStream_t st) {
+  const unsigned g = (unsigned)((L.n_fronts + kColsWarps - 1) / kColsWarps);
+  timer_begin(K_SOLVE_SMALL_BWD, st);
+  for (int col0 = 0; col0 < nrhs; col0 += 64) {
+    const int nr = std::min(64, nrhs - col0);
+    const bool two = nr > 32;
+#define TFB_COLS(K, P)                                                                        \
+  solve_bwd_cols<K, P><<<g, 32 * kColsWarps, 0, st>>>(L, PA, has_parent, factors, x_parent,     \
+                                                     parent_rows, x_out, out_rows, y, nr, nrhs, \
+                                                     col0)
+    if (L.max_k <= 4) { if (two) TFB_COLS(4, 2); else TFB_COLS(4, 1); }
+    else if (L.max_k <= 8) { if (two) TFB_COLS(8, 2); else TFB_COLS(8, 1); }
+    else { if (two) TFB_COLS(16, 2); else TFB_COLS(16, 1); }
+#undef TFB_COLS
+  }
+  timer_end(st);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_fwd_cols(const LevelArgs& L, const LevelArgs& O, int flag,
+                                   const double* factors, const double* w_in, long long in_rows,
+                                   double* w_out, long long out_rows, double* y, int nrhs,
+                                   cudaStream_t st) {
+  const unsigned g = (unsigned)((L.n_fronts + kColsWarps - 1) / kColsWarps);
+  timer_begin(K_SOLVE_SMALL_FWD, st);
+  for (int col0 = 0; col0 < nrhs; col0 += 64) {
+    const int nr = std::min(64, nrhs - col0);
+    const bool two = nr > 32;
+#define TFB_COLS(K, P)                                                                         \
+  solve_fwd_cols<K, P><<<g, 32 * kColsWarps, 0, st>>>(L, O, factors, w_in, in_rows, flag, w_out, \
+                                                      out_rows, y, nr, nrhs, col0)
+    if (L.max_k <= 4) { if (two) TFB_COLS(4, 2); else TFB_COLS(4, 1); }
+    else if (L.max_k <= 8) { if (two) TFB_COLS(8, 2); else TFB_COLS(8, 1); }
+    else { if (two) TFB_COLS(16, 2); else TFB_COLS(16, 1); }
+#undef TFB_COLS
+  }
+  timer_end(st);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- large fronts
 // Wavefront sweeps: one persistent launch per level and direction.  Work is
 // cut into 64x64 tiles of the fronts' panels; the tiles of the level are
@@ -1557,6 +1829,10 @@ static cudaError_t dispatch_small(const LevelArgs& L, const LevelArgs& O, int fl
                                   const double* factors, const double* w_in, long long in_rows,
                                   double* w_out, long long out_rows, double* y, int nrhs,
                                   cudaStream_t st) {
+  if (cols_solve_fwd(L, nrhs)) {
+    if (FWD) return launch_fwd_cols(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nrhs, st);
+    return launch_bwd_cols(L, O, flag, factors, w_in, in_rows, w_out, out_rows, y, nrhs, st);
+  }
   if (warp16_solve(L, nrhs)) {
     const size_t smem = (size_t)kSmallWarps * L.max_m * 8;
     const unsigned g = (unsigned)((L.n_fronts + kSmallWarps - 1) / kSmallWarps);
@@ -1837,6 +2113,7 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
 }
 
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
+  if (cols_solve_fwd(L, nrhs)) return (nrhs + 63) / 64;
   if (!level_is_large(L.is_leaf, L.max_m))
     return warp16_solve(L, nrhs) ? 1 : (nrhs + small_cols(L, nrhs) - 1) / small_cols(L, nrhs);
   if (narrow_solve(L, nrhs) || front_solve(L, nrhs, fwd)) return 1;
