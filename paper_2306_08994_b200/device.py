@@ -46,6 +46,9 @@ def _tri(n):
 # a stray write shows up in check_guards() and a read of unwritten data turns
 # the result into NaN.  Off by default (TFB_GUARD=1 or device.GUARD = True).
 GUARD = os.environ.get("TFB_GUARD", "0") == "1"
+# The public API (run_sequential / run_concurrent(1) / solve) replays cached
+# CUDA graphs of the whole factorization and solve (TFB_GRAPHS=0: eager).
+USE_GRAPHS = os.environ.get("TFB_GRAPHS", "1") != "0"
 GUARD_DOUBLES = 4096
 _CANARY = -0x0123456789ABCDF  # int64 bit pattern of the guard words (a NaN-free double)
 _guarded: list = []
@@ -203,6 +206,8 @@ class DevicePlan:
         self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
         self._solve_nrhs = 0
         self._blk = None
+        self._fgraph = None   # (threshold, CUDA graph) of factor() (public API path)
+        self._sgraphs = {}    # rhs shape -> (graph, static b, static x) of solve_into()
         self.fuse_bottom = True  # run the lowest levels as one subtree kernel when possible
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
@@ -357,6 +362,53 @@ class DevicePlan:
             self.solve_into(b, x, st)
         torch.cuda.current_stream(self.device).wait_stream(stream)
         return g
+
+    # ---- public-API path: cached CUDA graphs ------------------------------------
+    def _capture(self, fn) -> "torch.cuda.CUDAGraph":
+        cs = torch.cuda.Stream(self.device)
+        cs.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            fn(torch.cuda.current_stream(self.device))
+        torch.cuda.current_stream(self.device).wait_stream(cs)
+        return g
+
+    def factor_graphed(self, threshold: float) -> None:
+        """factor() on the current stream through a cached CUDA graph.
+
+        The first call runs eagerly (creating streams, kernel attributes and
+        buffers) and captures the launch sequence; later calls with the same
+        threshold replay it (the leaf values are read from `self.elem`, which
+        callers may overwrite in place).  Guard mode and TFB_GRAPHS=0 launch
+        eagerly every time."""
+        if not USE_GRAPHS or GUARD:
+            return self.factor(threshold)
+        if self._fgraph is not None and self._fgraph[0] == threshold:
+            self._fgraph[1].replay()
+            return
+        self.factor(threshold)
+        self._fgraph = (threshold, self._capture(lambda st: self.factor(threshold, st)))
+
+    def solve_graphed(self, b: torch.Tensor, x: torch.Tensor) -> None:
+        """solve_into() through a cached graph per column count, with static
+        right-hand-side / solution buffers (two device copies per call)."""
+        if not USE_GRAPHS or GUARD:
+            return self.solve_into(b, x)
+        shape = tuple(b.shape)
+        ent = self._sgraphs.get(shape)
+        if ent is None:
+            gb = torch.empty_like(b)
+            gx = torch.empty_like(b)
+            gb.copy_(b)
+            self.solve_into(gb, gx)
+            g = self._capture(lambda st: self.solve_into(gb, gx, st))
+            self._sgraphs[shape] = (g, gb, gx)
+            x.copy_(gx)
+            return
+        g, gb, gx = ent
+        gb.copy_(b)
+        g.replay()
+        x.copy_(gx)
 
     def launches_per_factor(self) -> int:
         """Kernel launches one factorization issues (tf_level_launch_count)."""

@@ -242,7 +242,7 @@ class FactorResult:
 
 def _factorize(plan, state: ExecState, compiled: Optional[DevicePlan] = None) -> FactorResult:
     dp = compiled or state.compiled or compile_execution(plan, None, state)
-    dp.factor(state.zero_threshold)
+    dp.factor_graphed(state.zero_threshold)
     pos = dp.zero_pivot_position()
     if pos >= 0:
         front, pivot = plan.locate_pivot(pos)
@@ -335,7 +335,7 @@ def solve(factors: FactorResult, rhs):
             raise ValueError(f"rhs must have length {n}, got {arr.shape}")
     b = _as_device(rhs, dp.device, n)
     x = torch.empty_like(b)
-    dp.solve_into(b, x)
+    dp.solve_graphed(b, x)
     if isinstance(rhs, torch.Tensor):
         return x
     return x.cpu().numpy()
