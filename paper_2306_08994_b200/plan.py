@@ -8,7 +8,10 @@ tasks.py:88-159): pivot order, per-level front patterns and extend-add maps.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
+import os
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
@@ -48,12 +51,83 @@ class LevelTables:
         return np.bincount(self.pattern_of, minlength=self.n_patterns)
 
 
+PLAN_CACHE_VERSION = 1
+_SCALARS = ("n_dof", "n_leaves", "n_nodes", "n_pivots", "n_levels", "max_m", "max_k")
+_LEVEL_FIELDS = ("level", "n_fronts", "node_base", "piv_base", "n_pivots", "max_m", "max_k",
+                 "max_upd")
+_LEVEL_ARRAYS = ("pattern_of", "piv_off", "pat", "maps")
+
+
+def plan_cache_path(fronts: FrontSet, n_dof: int, cache_dir) -> Path:
+    """Cache file of the plan of these leaf fronts: keyed by a digest of n_dof, the
+    front index lists (in order) and the cache format version."""
+    h = hashlib.sha256()
+    h.update(f"tfb-plan-v{PLAN_CACHE_VERSION}:{int(n_dof)}:{len(fronts)}".encode())
+    h.update(np.ascontiguousarray(fronts.dofs, dtype=np.int32).tobytes())
+    if fronts.ptr is not None:
+        h.update(np.ascontiguousarray(fronts.ptr, dtype=np.int64).tobytes())
+    return Path(cache_dir) / f"plan_{h.hexdigest()[:32]}.npz"
+
+
 class NativePlan:
-    def __init__(self, fronts: FrontSet, n_dof: int, keep_lists: bool = False):
+    """The symbolic plan (tree, pivot order, level tables) of a set of leaf fronts.
+
+    With `cache_dir` (or TFB_PLAN_CACHE) and without per-node lists, the plan is
+    stored on disk after it is built and loaded from there the next time the
+    same fronts are planned (cfg5: ~20 s of symbolic work -> one file read);
+    a cached plan carries no native handle (node lists / atomic FNF need
+    keep_lists, which is never cached)."""
+
+    def __init__(self, fronts: FrontSet, n_dof: int, keep_lists: bool = False, cache_dir=None):
         if len(fronts) == 0:
             raise EmptyInputError("cannot build a tree from zero fronts")
         lib = _lib.load()
         self._lib = lib
+        self._h = C.c_void_p()
+        cache_dir = cache_dir if cache_dir is not None else os.environ.get("TFB_PLAN_CACHE")
+        path = plan_cache_path(fronts, n_dof, cache_dir) if cache_dir and not keep_lists else None
+        self.cache_hit = False
+        if path is not None and path.exists():
+            try:
+                self._load(path)
+                self.cache_hit = True
+                return
+            except Exception:
+                pass  # unreadable / stale: rebuild below and overwrite
+        self._build(fronts, n_dof, keep_lists)
+        if path is not None:
+            self._save(path)
+
+    def _save(self, path: Path) -> None:
+        d = {k: np.int64(getattr(self, k)) for k in _SCALARS}
+        d["pivot_order"] = self.pivot_order
+        d["n_level_tables"] = np.int64(len(self.levels))
+        for L, lt in enumerate(self.levels):
+            for k in _LEVEL_FIELDS:
+                d[f"L{L}_{k}"] = np.int64(getattr(lt, k))
+            for k in _LEVEL_ARRAYS:
+                d[f"L{L}_{k}"] = getattr(lt, k)
+        path.parent.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_name(path.name + f".{os.getpid()}.tmp")
+        with open(tmp, "wb") as fh:
+            np.savez(fh, **d)
+        os.replace(tmp, path)
+
+    def _load(self, path: Path) -> None:
+        with np.load(path) as z:
+            for k in _SCALARS:
+                setattr(self, k, int(z[k]))
+            self.keep_lists = False
+            self.pivot_order = z["pivot_order"].astype(np.int32)
+            levels = []
+            for L in range(int(z["n_level_tables"])):
+                kw = {k: int(z[f"L{L}_{k}"]) for k in _LEVEL_FIELDS}
+                kw.update({k: z[f"L{L}_{k}"] for k in _LEVEL_ARRAYS})
+                levels.append(LevelTables(**kw))
+            self.levels = levels
+
+    def _build(self, fronts: FrontSet, n_dof: int, keep_lists: bool) -> None:
+        lib = self._lib
         h = C.c_void_p()
         dofs = np.ascontiguousarray(fronts.dofs, dtype=np.int32)
         if fronts.ptr is None:
@@ -85,7 +159,7 @@ class NativePlan:
 
     def atomic_fnf(self):
         """(FnfStats, widths[int64], kinds[int32]) of the atomic Foata normal form."""
-        if not self.keep_lists:
+        if not self.keep_lists or not self._h.value:
             raise RuntimeError("atomic FNF needs a plan built with keep_lists")
         st = _lib.FnfStats()
         rc = self._lib.tf_atomic_fnf(self._h, C.byref(st), None, None, 0)

@@ -72,12 +72,13 @@ def join_fronts(left: Front, right: Front, new_id: int = -1,
 class EliminationTree:
     """Elimination tree over leaf fronts (tree.py:28-41), backed by a NativePlan."""
 
-    def __init__(self, fronts: FrontSet, n_dof: Optional[int] = None, keep_lists: bool = None):
+    def __init__(self, fronts: FrontSet, n_dof: Optional[int] = None, keep_lists: bool = None,
+                 cache_dir=None):
         self.fronts = fronts
         self.n_dof = _n_dof_of(fronts) if n_dof is None else int(n_dof)
         if keep_lists is None:
             keep_lists = len(fronts) <= MATERIALIZE_LIMIT
-        self.plan = NativePlan(fronts, self.n_dof, keep_lists=keep_lists)
+        self.plan = NativePlan(fronts, self.n_dof, keep_lists=keep_lists, cache_dir=cache_dir)
         sizes = [lt.n_fronts for lt in self.plan.levels]
         bases = np.concatenate([[0], np.cumsum(sizes)])
         self.level_sizes = tuple(sizes)
