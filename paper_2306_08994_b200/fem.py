@@ -136,9 +136,10 @@ class Mesh:
         return element_mass_matrix(self.element_width, self.degree)
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, eq=False)
 class TensorMesh:
-    """Uniform tensor-product Q_p mesh of the unit box in 1, 2 or 3 dimensions.
+    """Tensor-product Q_p mesh of the unit box in 1, 2 or 3 dimensions (uniform, or
+    graded through per-axis `nodes` and weighted by a per-element `density`).
 
     DOFs are numbered by the Morton index of their owning element (grid point
     i on an axis with n elements belongs to element min(i//p, n-1)); elements
@@ -151,11 +152,40 @@ class TensorMesh:
 
     shape: tuple[int, ...]
     degree: int
+    # Optional non-uniform data: per-axis element
+    # boundaries (n_a + 1 increasing values from 0 to 1: a graded mesh) and a
+    # per-element density (Morton element order) scaling each element matrix.
+    nodes: Optional[tuple] = None
+    density: Optional[np.ndarray] = None
 
     def __post_init__(self) -> None:
         if not 1 <= len(self.shape) <= 3 or any(n < 1 for n in self.shape):
             raise InvalidGeometryError(f"invalid mesh shape {self.shape}")
         _check_degree(self.degree)
+        if self.nodes is not None:
+            nodes = tuple(np.asarray(x, dtype=np.float64) for x in self.nodes)
+            if len(nodes) != len(self.shape) or any(
+                    len(x) != n + 1 or x[0] != 0.0 or x[-1] != 1.0 or np.any(np.diff(x) <= 0)
+                    for x, n in zip(nodes, self.shape)):
+                raise InvalidGeometryError("nodes: per axis n+1 increasing values from 0 to 1")
+            object.__setattr__(self, "nodes", nodes)
+        if self.density is not None:
+            rho = np.asarray(self.density, dtype=np.float64).ravel()
+            if len(rho) != self.n_elements or np.any(rho <= 0):
+                raise InvalidGeometryError("density: one positive value per element")
+            object.__setattr__(self, "density", rho)
+
+    @property
+    def uniform(self) -> bool:
+        return self.nodes is None and self.density is None
+
+    def _widths(self, a: int) -> np.ndarray:
+        n = self.shape[a]
+        return np.full(n, 1.0 / n) if self.nodes is None else np.diff(self.nodes[a])
+
+    def _offsets(self, a: int) -> np.ndarray:
+        n = self.shape[a]
+        return np.arange(n) / n if self.nodes is None else self.nodes[a][:-1]
 
     @property
     def dim(self) -> int:
@@ -189,11 +219,31 @@ class TensorMesh:
         return out
 
     def element_matrix(self) -> np.ndarray:
+        """The uniform element matrix (or, for a non-uniform mesh, the stack of
+        per-element matrices in Morton order: `element_values`)."""
+        if not self.uniform:
+            return self.element_values()
         mats = [element_mass_matrix(1.0 / n, self.degree) for n in self.shape]
         out = mats[0]
         for m in mats[1:]:
             out = np.kron(m, out)
         return out
+
+    def element_values(self) -> np.ndarray:
+        """Per-element matrices (n_elements, nloc, nloc): kron of the 1D mass
+        matrices of each element's widths (fem.py:108-114 per axis), times its
+        density.  M_e(h) = h M_e(1), so each is a scaled reference matrix."""
+        ref = [element_mass_matrix(1.0, self.degree) for _ in self.shape]
+        out = ref[0]
+        for m in ref[1:]:
+            out = np.kron(m, out)
+        coords = self.element_coords()
+        scale = np.ones(len(coords))
+        for a in range(self.dim):
+            scale *= self._widths(a)[coords[:, a]]
+        if self.density is not None:
+            scale *= self.density
+        return scale[:, None, None] * out[None, :, :]
 
     def element_coords(self) -> np.ndarray:
         """(n_elements, d) integer element coordinates in Morton order."""
@@ -212,9 +262,9 @@ class TensorMesh:
         f1 = RHS_FUNCTIONS[rhs_name]
         p = self.degree
         per_axis = []
-        for n in self.shape:
-            h = 1.0 / n
-            per_axis.append(np.array([element_load_vector(h, p, f1, e * h) for e in range(n)]))
+        for a, n in enumerate(self.shape):
+            hs, xs = self._widths(a), self._offsets(a)
+            per_axis.append(np.array([element_load_vector(hs[e], p, f1, xs[e]) for e in range(n)]))
         coords = self.element_coords()
         loads = per_axis[0][coords[:, 0]]
         for a in range(1, self.dim):
@@ -513,6 +563,20 @@ def _tensor_peak(mesh: TensorMesh) -> float:
     return ElementSystem(patch.n_dof, fs, np.zeros(patch.n_dof)).peak
 
 
+def _element_peak(fs: FrontSet, n_dof: int) -> float:
+    """max|A_ij| of the element assembly, vectorised (non-uniform element values)."""
+    d = fs.dofs.astype(np.int64)
+    nloc = d.shape[1]
+    vals = np.broadcast_to(fs.values, (len(d), nloc, nloc)) if fs.uniform_values else fs.values
+    ia = np.repeat(d, nloc, axis=1).ravel()
+    ib = np.tile(d, (1, nloc)).ravel()
+    keep = ia >= ib
+    key = ia[keep] * (n_dof + 1) + ib[keep]
+    uniq, inv = np.unique(key, return_inverse=True)
+    sums = np.bincount(inv, weights=vals.reshape(len(d), -1).ravel()[keep], minlength=len(uniq))
+    return float(np.abs(sums).max()) if len(sums) else 0.0
+
+
 def assemble_system(mesh, f: Callable[[float], float] | str = "one") -> GlobalSystem:
     """Global system M u = b (fem.py:218-232).
 
@@ -523,7 +587,8 @@ def assemble_system(mesh, f: Callable[[float], float] | str = "one") -> GlobalSy
     if isinstance(mesh, TensorMesh):
         name = f if isinstance(f, str) else next(k for k, v in RHS_FUNCTIONS.items() if v is f)
         fs = generate_fronts(mesh)
-        return ElementSystem(mesh.n_dof, fs, mesh.load_vector(name), peak=_tensor_peak(mesh))
+        peak = _tensor_peak(mesh) if mesh.uniform else _element_peak(fs, mesh.n_dof)
+        return ElementSystem(mesh.n_dof, fs, mesh.load_vector(name), peak=peak)
     func = RHS_FUNCTIONS[f] if isinstance(f, str) else f
     system = GlobalSystem(n_dof=mesh.n_dof, rhs=np.zeros(mesh.n_dof))
     h = mesh.element_width

@@ -20,7 +20,7 @@ def golden(name):
 
 
 def golden_names():
-    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("scale_"))
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith(("scale_", "symbolic_")))
 
 
 def mesh_of(g):
