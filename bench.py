@@ -371,11 +371,13 @@ def run_ours(args, cfg):
             asm_bytes += st["bytes"] - 8.0 * st["upd_entries"]
         else:
             small_bytes += st["bytes"]
-    # solve sweeps (per direction): factor entries read once + the front
-    # vector blocks written and read (8 B x nrhs per front row, twice)
+    # solve sweeps (per direction): algorithmic bytes of each level
     solve_small = solve_large = 0.0
     for L, (dl, st) in enumerate(zip(dp.levels, stats)):
-        b_ = 8.0 * st["fac_entries"] + 16.0 * nrhs * float(dl.tables.front_m().sum())
+        # factor entries read once per sweep + each pivot's RHS row
+        # read and written once (the update blocks passed between levels are
+        # layout traffic, not algorithmic work)
+        b_ = 8.0 * st["fac_entries"] + 16.0 * nrhs * float(st["pivots"])
         if large[L]:
             solve_large += b_
         else:
