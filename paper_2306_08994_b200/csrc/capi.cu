@@ -11,6 +11,7 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
                                 double* upd_out, double thr, unsigned long long* err,
                                 int* ws_flags, cudaStream_t st);
 bool root_dataflow_level(const LevelArgs& L);
+long long level_factor_ws_ints(const LevelArgs& L);
 cudaError_t launch_solve_fwd(const LevelArgs& L, const LevelArgs& C, const double* factors,
                              const double* w_child, long long child_rows, double* w_out,
                              long long out_rows, double* y, int nrhs, double* work,
@@ -47,11 +48,11 @@ extern "C" int64_t tf_level_aux_doubles(const tf_level_view* lv) {
 }
 
 extern "C" int64_t tf_level_factor_workspace(const tf_level_view* lv) {
-  // the root-dataflow kernel's acquire/release flags: one set per caller-owned
-  // workspace, so concurrent factorizations never share them
+  // the dataflow kernels' acquire/release flags (root; lookahead chains): one
+  // set per caller-owned workspace, so concurrent factorizations never share them
   if (!lv || lv->n_fronts == 0 || !level_is_large(lv->is_leaf, lv->max_m)) return 0;
   const LevelArgs L = make_args(lv);
-  return root_dataflow_level(L) ? (int64_t)sizeof(int) * root_flag_ints(L) : 0;
+  return (int64_t)sizeof(int) * level_factor_ws_ints(L);
 }
 
 extern "C" int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs) {

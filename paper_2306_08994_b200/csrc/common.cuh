@@ -108,11 +108,6 @@ inline LevelArgs make_args(const tf_level_view* v) {
   return a;
 }
 
-// Root-dataflow flag words of a level (factor workspace, tf_level_factor_workspace)
-inline long long root_flag_ints(const LevelArgs& L) {
-  const long long T = (L.max_k + 63) / 64, nf = L.n_fronts;
-  return nf * T * T + 2 * nf * T + 1 + nf;
-}
 
 // Per-front view of the pattern row.
 struct Shape {

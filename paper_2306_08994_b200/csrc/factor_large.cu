@@ -933,9 +933,21 @@ static int schur_group() {  // TFB_SCHUR_GROUP (tuning)
   return v;
 }
 
+static bool chain_dataflow() {  // TFB_CHAIN_DATAFLOW: lookahead chains as dataflow launches
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TFB_CHAIN_DATAFLOW");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
+static cudaError_t launch_dataflow(const LevelArgs& L, double* factors, double thr,
+                                   unsigned long long* err, int* ws_flags, int cb0, int TC,
+                                   int TR, bool coop, cudaStream_t st);
+
 static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd, double* factors,
-                                    double* upd_out,
-                                    double thr, unsigned long long* err, cudaStream_t st) {
+                                    double* upd_out, double thr, unsigned long long* err,
+                                    int* ws_flags, cudaStream_t st) {
   LookaheadStreams& S = lookahead_streams();
   cudaEventRecord(S.start, st);  // after the assembly
   cudaStreamWaitEvent(S.chain, S.start, 0);
@@ -947,7 +959,15 @@ static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd,
   for (int j = 0; j < nsb; j++) {
     const int c0 = j * W, c1 = std::min(c0 + W, L.max_k);
     const int c2 = std::min(c1 + W, L.max_k);
-    cudaError_t e = panel_factor(L, factors, thr, err, c0, c1, S.chain);
+    cudaError_t e;
+    if (chain_dataflow() && L.max_upd > 0) {
+      // the super-block's whole chain (diagonal blocks, sub-diagonal and row
+      // tiles down to m) as one dataflow launch
+      const int TC = (c1 - c0 + NB - 1) / NB, TR = (L.max_m - c0 + NB - 1) / NB;
+      e = launch_dataflow(L, factors, thr, err, ws_flags, c0, TC, TR, false, S.chain);
+    } else {
+      e = panel_factor(L, factors, thr, err, c0, c1, S.chain);
+    }
     if (e != cudaSuccess) return e;
     if (j + 1 < nsb) {
       // the panel stream's update by j-1 covers columns >= c1: it must land first
@@ -995,6 +1015,20 @@ static bool root_dataflow() {  // TFB_ROOT_DATAFLOW=0 selects the lookahead path
 
 bool root_dataflow_level(const LevelArgs& L) {
   return L.max_upd == 0 && L.max_k > 0 && root_dataflow();
+}
+
+static inline long long flag_ints(long long nf, int TR, int TC) {
+  return nf * TR * TC + 2 * nf * (TC + 1) + 1 + nf;
+}
+// Flag words the level's dataflow launches need (tf_level_factor_workspace).
+long long level_factor_ws_ints(const LevelArgs& L) {
+  const int T = (L.max_k + NB - 1) / NB;
+  if (root_dataflow_level(L)) return flag_ints(L.n_fronts, T, T);
+  const int W = lookahead_width(L.max_upd);
+  if (chain_dataflow() && L.max_upd > 0 && L.max_k > W &&
+      L.level_fronts <= kLookaheadMaxFronts)
+    return flag_ints(L.n_fronts, (L.max_m + NB - 1) / NB, (W + NB - 1) / NB);
+  return 0;
 }
 
 // ------------------------------------------------------------- root fronts
@@ -1115,7 +1149,7 @@ __device__ __forceinline__ void root_trsm_rows(double (&x)[8][2], double (*S)[DL
 
 // The pivot chain of front f (one CTA).
 __device__ void root_chain(const LevelArgs& L, double* factors, double threshold,
-                           unsigned long long* err, long long f, int T, int* done,
+                           unsigned long long* err, long long f, int cb0, int TC, int* done,
                            const int* part_diag, const int* part_sub, long long* trace) {
   extern __shared__ __align__(16) double rsm[];
   __shared__ int s_ready;
@@ -1126,7 +1160,8 @@ __device__ void root_chain(const LevelArgs& L, double* factors, double threshold
   double* dprev = dv + NB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g8 = lane >> 2, tq = lane & 3;
   const Shape s = front_shape(L, f);
-  const int k = s.k, kp = s.kp;
+  const int k = s.k, kp = s.kp, m = s.m;
+  const int kend = min(k, cb0 + TC * NB);  // this launch's pivot columns [cb0, kend)
   double* Pf = factors + f * L.fac_stride;
   double* dvec = Pf + (long long)s.m * kp;
   // rows [row0, row0 + nr) x columns [col0, col0 + nc) of the panel into X
@@ -1144,10 +1179,11 @@ __device__ void root_chain(const LevelArgs& L, double* factors, double threshold
     if (tid == 0) s_ready = want ? ld_acquire_gpu(flag) : 0;
   };
   bool d_pref = false;
-  for (int l = 0; l < T; l++) {
-    const int c0 = l * NB, kb = min(NB, k - c0);
+  for (int l = 0; l < TC; l++) {
+    const int c0 = cb0 + l * NB, kb = min(NB, kend - c0);
     if (kb <= 0) break;
-    const int r0 = c0 + NB, nA = min(NB, k - r0);
+    const int r0 = c0 + NB, nA = min(NB, m - r0);  // sub-diagonal tile rows
+    const int kn = min(NB, kend - r0);             // next diagonal block (<= 0: none)
     if (!d_pref) {
       if (tid == 0) root_wait(part_diag + l);
       __syncthreads();
@@ -1195,43 +1231,51 @@ __device__ void root_chain(const LevelArgs& L, double* factors, double threshold
       __syncthreads();  // every 1/d read
       if (tid < NB) dprev[tid] = dv[tid];
       __syncthreads();
-      root_publish(done + (l + 1) * T + l);
+      root_publish(done + (l + 1) * TC + l);
       if (trace && tid == 0) trace[l * 8 + 2] = root_clock();
     }
     // d and the aux block (M_l for the other tiles' solves), then the panel
-    write_aux64<256>(L.aux + f * L.aux_stride + (long long)l * NB * NB, D, Mi, dv, kb);
+    write_aux64<256>(L.aux + f * L.aux_stride + (long long)(c0 / NB) * NB * NB, D, Mi, dv, kb);
     for (int c = tid; c < kb; c += 256) {
       dvec[c0 + c] = dv[c];
       if (fabs(dv[c]) <= threshold)
         record_zero_pivot(err, (unsigned long long)(L.piv_off[f] + c0 + c));
     }
     __syncthreads();
-    root_publish(done + l * T + l);
+    root_publish(done + l * TC + l);
     for (int e = tid; e < NB * NB; e += 256) {
       const int a = e >> 6, b = e & 63;
       if (a < kb && b <= a) Pf[(long long)(c0 + a) * kp + c0 + b] = D[a][b];
     }
     if (trace && tid == 0) trace[l * 8 + 3] = root_clock();
     // prefetch the next partial diagonal tile when it is ready
-    probe(part_diag + l + 1, nA > 0);
+    probe(part_diag + l + 1, kn > 0);
     __syncthreads();  // also: D fully read
     d_pref = s_ready != 0;
-    if (d_pref) load_tile(D, r0, nA, r0, nA);
+    if (d_pref) load_tile(D, r0, kn, r0, kn);
   }
+}
+
+// flags of one launch over column blocks [cb0/64, cb0/64 + TC) and row blocks
+// [cb0/64, cb0/64 + TR): done[nf][TR][TC], part_diag[nf][TC+1],
+// part_sub[nf][TC+1], counter, chain_sm[nf]
+inline long long chain_flag_ints(long long nf, int TR, int TC) {
+  return nf * TR * TC + 2 * nf * (TC + 1) + 1 + nf;
 }
 
 __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double* factors,
                                                          double threshold,
                                                          unsigned long long* err, int* flags,
-                                                         int T, long long* trace) {
+                                                         int cb0, int TC, int TR,
+                                                         long long* trace) {
   constexpr int BK = GRoot::BK, ST = GRoot::ST, LD = GRoot::LD, MI = GRoot::MI, NJ = GRoot::NJ;
   extern __shared__ __align__(16) double rsm[];
   __shared__ int s_tile;
   const int nf = L.n_fronts;
-  int* done = flags;                               // [nf][T][T] final tiles
-  int* part_diag = done + (long long)nf * T * T;   // [nf][T] partial diagonal tiles
-  int* part_sub = part_diag + (long long)nf * T;   // [nf][T] partial sub-diagonal tiles
-  int* counter = part_sub + (long long)nf * T;
+  int* done = flags;                                     // [nf][TR][TC] final tiles
+  int* part_diag = done + (long long)nf * TR * TC;       // [nf][TC+1] partial diagonal tiles
+  int* part_sub = part_diag + (long long)nf * (TC + 1);  // [nf][TC+1] partial sub-diagonal
+  int* counter = part_sub + (long long)nf * (TC + 1);
   int* chain_sm = counter + 1;  // [nf] SM of each chain CTA, + 1 (0: not yet known)
   if (blockIdx.x < (unsigned)nf) {
     if (threadIdx.x == 0) {
@@ -1239,9 +1283,9 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
       st_release_gpu(chain_sm + blockIdx.x, (int)sm + 1);
     }
-    root_chain(L, factors, threshold, err, blockIdx.x, T, done + (long long)blockIdx.x * T * T,
-               part_diag + (long long)blockIdx.x * T, part_sub + (long long)blockIdx.x * T,
-               blockIdx.x == 0 ? trace : nullptr);
+    root_chain(L, factors, threshold, err, blockIdx.x, cb0, TC,
+               done + (long long)blockIdx.x * TR * TC, part_diag + (long long)blockIdx.x * (TC + 1),
+               part_sub + (long long)blockIdx.x * (TC + 1), blockIdx.x == 0 ? trace : nullptr);
     return;
   }
   double* As = rsm;  // GEMM staging [ST][64][LD], [ST][64][LD], [ST][BK]
@@ -1252,7 +1296,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
   double* dv = rsm + 2 * NB * DLD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wy = warp / GRoot::WC, wx = warp % GRoot::WC, g8 = lane >> 2, tq = lane & 3;
-  const long long ntiles = (long long)T * (T + 1) / 2 * nf;
+  const long long ntiles = ((long long)TC * TR - (long long)TC * (TC - 1) / 2) * nf;
   // tile CTAs leave the chain CTAs' SMs to them (the chain is the critical path)
   if (tid == 0) {
     unsigned sm;
@@ -1277,16 +1321,17 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
     const long long f = t % nf;
     long long rr = t / nf;
     int l = 0;
-    while (rr >= T - l) rr -= T - l++;
+    while (rr >= TR - l) rr -= TR - l++;
     const int i = l + (int)rr;
     const Shape s = front_shape(L, f);
-    const int k = s.k, kp = s.kp;
-    const int r0 = i * NB, c0 = l * NB;
-    if (r0 >= k) continue;  // beyond this front (smaller than the level's largest)
-    const int nA = min(NB, k - r0), nB = min(NB, k - c0);
+    const int k = s.k, kp = s.kp, m = s.m;
+    const int kend = min(k, cb0 + TC * NB);
+    const int r0 = cb0 + i * NB, c0 = cb0 + l * NB;
+    if (r0 >= m || c0 >= kend) continue;  // beyond this front (smaller than the level's largest)
+    const int nA = min(NB, m - r0), nB = min(NB, kend - c0);
     double* Pf = factors + f * L.fac_stride;
     const double* dvec = Pf + (long long)s.m * kp;
-    int* fl = done + f * T * T;
+    int* fl = done + f * TR * TC;
     // the chain applies the last column to the diagonal tile itself
     const int ncols = i == l ? max(l - 1, 0) : l;
     const int nk = ncols * (NB / BK);
@@ -1300,17 +1345,17 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
       for (int q = 0; q < (NB * CPR) / 256; q++) {
         const int ch = tid + q * 256, r = ch / CPR, cc = (ch % CPR) * 2;
         const bool va = r < nA, vb = r < nB;
-        cp_async16(as + r * LD + cc, va ? Pf + (long long)(r0 + r) * kp + kt + cc : Pf, va);
-        cp_async16(bs + r * LD + cc, vb ? Pf + (long long)(c0 + r) * kp + kt + cc : Pf, vb);
+        cp_async16(as + r * LD + cc, va ? Pf + (long long)(r0 + r) * kp + cb0 + kt + cc : Pf, va);
+        cp_async16(bs + r * LD + cc, vb ? Pf + (long long)(c0 + r) * kp + cb0 + kt + cc : Pf, vb);
       }
-      if (tid < CPR) cp_async16(Ds + stage * BK + tid * 2, dvec + kt + tid * 2, true);
+      if (tid < CPR) cp_async16(Ds + stage * BK + tid * 2, dvec + cb0 + kt + tid * 2, true);
     };
     // column j of the product is ready once tiles (i, j) and (l, j) are final
     auto wait_col = [&](int it) {
       if (tid == 0 && (it % (NB / BK)) == 0) {
         const int j = it / (NB / BK);
-        root_wait(fl + i * T + j);
-        if (i != l) root_wait(fl + l * T + j);
+        root_wait(fl + i * TC + j);
+        if (i != l) root_wait(fl + l * TC + j);
       }
     };
 
@@ -1367,7 +1412,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
             }
       }
       __syncthreads();
-      root_publish(i == l ? part_diag + f * T + l : part_sub + f * T + i);
+      root_publish(i == l ? part_diag + f * (TC + 1) + l : part_sub + f * (TC + 1) + i);
       continue;
     }
     // A = assembled tile - product, into D
@@ -1382,9 +1427,9 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
                                            : 0.0;
         }
     // L_il = A M_l^T D_l^-1 (M_l: strict lower part of the published aux block)
-    if (tid == 0) root_wait(fl + l * T + l);
+    if (tid == 0) root_wait(fl + l * TC + l);
     __syncthreads();
-    const double* M = L.aux + f * L.aux_stride + (long long)l * NB * NB;
+    const double* M = L.aux + f * L.aux_stride + (long long)(c0 / NB) * NB * NB;
     for (int e = tid; e < NB * NB; e += 256) {
       const int a = e >> 6, b = e & 63;
       Mi[a][b] = b < a ? M[e] : (b == a ? 1.0 : 0.0);
@@ -1403,7 +1448,7 @@ __global__ void __launch_bounds__(256, 2) large_root_kernel(LevelArgs L, double*
           if (rl < nA && cl < nB) Pf[(long long)(r0 + rl) * kp + c0 + cl] = x[a][b][h] * dv[cl];
         }
     __syncthreads();
-    root_publish(fl + i * T + l);
+    root_publish(fl + i * TC + l);
   }
 }
 
@@ -1423,11 +1468,27 @@ static int* root_flags(long long ints) {  // per-device scratch, grown on demand
   return buf[dev];
 }
 
+static cudaError_t launch_dataflow(const LevelArgs& L, double* factors, double thr,
+                                   unsigned long long* err, int* ws_flags, int cb0, int TC,
+                                   int TR, bool coop, cudaStream_t st);
+
 static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
                                unsigned long long* err, int* ws_flags, cudaStream_t st) {
   const int T = (L.max_k + NB - 1) / NB;
+  return launch_dataflow(L, factors, thr, err, ws_flags, 0, T, T, true, st);
+}
+
+// The pivot columns [cb0, cb0 + 64 TC) of every front of a level as one
+// dataflow launch (root kernel): one chain CTA per front factors the diagonal
+// blocks and their sub-diagonal tiles; tile CTAs take the other panel tiles
+// (rows down to m) left-looking over the launch's own columns.  Lookahead
+// super-blocks use it with the columns before cb0 already applied.
+static cudaError_t launch_dataflow(const LevelArgs& L, double* factors, double thr,
+                                   unsigned long long* err, int* ws_flags, int cb0, int TC,
+                                   int TR, bool coop, cudaStream_t st) {
+  const int T = TC;
   const long long nf = L.n_fronts;
-  const long long nflags = root_flag_ints(L);
+  const long long nflags = chain_flag_ints(nf, TR, TC);
   // the caller's workspace (one per DevicePlan level), else a per-device scratch
   int* flags = ws_flags ? ws_flags : root_flags(nflags);
   if (!flags) return cudaErrorMemoryAllocation;
@@ -1444,7 +1505,7 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // chain CTAs + tile CTAs, all co-resident (tile CTAs wait on the chain)
-  const long long ntiles = nf * T * (T + 1) / 2;
+  const long long ntiles = nf * ((long long)TC * TR - (long long)TC * (TC - 1) / 2);
   const long long cap = (long long)sms * occ;
   // tile CTAs that land next to a chain CTA exit: keep at least one other
   if (nf * occ + 1 > cap) return cudaErrorInvalidConfiguration;
@@ -1455,8 +1516,18 @@ static cudaError_t factor_root(const LevelArgs& L, double* factors, double thr,
     cudaMemset(trace, 0, sizeof(long long) * 8 * 4096);
   }
   timer_begin(K_ROOT, st);
-  e = launch_cooperative(large_root_kernel, dim3(grid), dim3(256), kRootSmem, st, L, factors, thr,
-                         err, flags, T, trace);
+  if (coop) {
+    e = launch_cooperative(large_root_kernel, dim3(grid), dim3(256), kRootSmem, st, L, factors,
+                           thr, err, flags, cb0, TC, TR, trace);
+  } else {
+    // concurrent with the lookahead Schur stream: a cooperative grid would wait
+    // for the whole grid's worth of free slots.  Progress without co-residency:
+    // the chain CTAs are the lowest block indices (dispatched first) and a tile
+    // CTA only waits on the chain or on tiles dealt before it.
+    large_root_kernel<<<grid, 256, kRootSmem, st>>>(L, factors, thr, err, flags, cb0, TC, TR,
+                                                     trace);
+    e = cudaGetLastError();
+  }
   timer_end(st);
   if (e != cudaSuccess) return e;
   if (trace && T <= 4096) {
@@ -1508,7 +1579,7 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
   if (e != cudaSuccess) return e;
   if (L.max_upd == 0 && L.max_k > 0 && root_dataflow())
     return factor_root(L, factors, thr, err, ws_flags, st);
-  if (lookahead) return factor_lookahead(L, child_upd, factors, upd_out, thr, err, st);
+  if (lookahead) return factor_lookahead(L, child_upd, factors, upd_out, thr, err, ws_flags, st);
   if (L.max_k > 0) {
     e = panel_factor(L, factors, thr, err, 0, L.max_k, st);
     if (e != cudaSuccess) return e;
