@@ -59,6 +59,28 @@ extern "C" {
 int tf_mesh_tensor(int32_t dim, const int64_t* ns, int32_t degree, int64_t* n_dof,
                    int64_t* n_elem, int32_t* elem_dofs);
 
+/* tf_mesh_tensor on the GPU (same tables, bitwise): Morton keys, a radix sort,
+ * an exclusive scan of owned-point counts and one thread per (element, local
+ * point).  elem_dofs: device, n_elem * (p+1)^dim int32; order_out (optional,
+ * device, n_elem int64): the x-fastest linear index of each Morton-ordered
+ * element.  workspace: tf_mesh_tensor_device_workspace() bytes of device
+ * memory.  Replaces the element loop of fem.py:59-80 / generate_fronts
+ * (fem.py:235-259) for tensor meshes. */
+int64_t tf_mesh_tensor_device_workspace(int32_t dim, const int64_t* ns, int32_t degree);
+int tf_mesh_tensor_device(int32_t dim, const int64_t* ns, int32_t degree, int32_t* elem_dofs,
+                          int64_t* order_out, void* workspace, int64_t workspace_bytes,
+                          void* stream);
+
+/* Element matrices of a graded / weighted tensor mesh on the GPU, Morton
+ * order: values[e] = (prod_a width_a(e)) * density[e] * ref (ref = kron of the
+ * reference 1D mass matrices of unit width, fem.py:108-114).  nodes: device,
+ * concatenated per-axis element boundaries (n_a + 1 each) or NULL (uniform);
+ * density: device, per Morton element, or NULL. */
+int tf_mesh_element_values_device(int32_t dim, const int64_t* ns, int32_t degree,
+                                  const int64_t* order, const double* nodes,
+                                  const double* density, const double* ref, double* values,
+                                  void* stream);
+
 /* -------------------------------------------------------------- symbolic */
 
 typedef struct tf_plan tf_plan;

@@ -175,10 +175,16 @@ class DevicePlan:
         native = plan.native
         self.n_dof = plan.n_dof
         self.n_pivots = native.n_pivots
-        vals = np.ascontiguousarray(fronts.values if values is None else values, dtype=np.float64)
-        elem_ld = vals.shape[-1]
-        elem_stride = 0 if vals.ndim == 2 else elem_ld * elem_ld
-        self.elem = torch.from_numpy(vals.ravel()).to(self.device)
+        if isinstance(values, torch.Tensor):  # generated on the device (meshgen)
+            elem_ld = int(values.shape[-1])
+            elem_stride = 0 if values.dim() == 2 else elem_ld * elem_ld
+            self.elem = values.to(device=self.device, dtype=torch.float64).reshape(-1).contiguous()
+        else:
+            vals = np.ascontiguousarray(fronts.values if values is None else values,
+                                        dtype=np.float64)
+            elem_ld = vals.shape[-1]
+            elem_stride = 0 if vals.ndim == 2 else elem_ld * elem_ld
+            self.elem = torch.from_numpy(vals.ravel()).to(self.device)
         self.levels: list[DeviceLevel] = []
         child = 0
         zprev = None
