@@ -17,6 +17,7 @@
 // children's shared sets, laid out [eliminable ascending | shared ascending]
 // exactly like NodeReorder (tasks.py:114-130).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -58,6 +59,16 @@ struct tf_plan {
   std::vector<int32_t> pivot_order;
   std::vector<Level> levels;
 };
+
+static int kp_align() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("TFB_KP_ALIGN");
+    v = e ? atoi(e) : 2;
+    if (v != 2 && v != 4) v = 2;
+  }
+  return v;
+}
 
 extern "C" int tf_mesh_tensor(int32_t dim, const int64_t* ns, int32_t p, int64_t* n_dof_out,
                               int64_t* n_elem_out, int32_t* elem_dofs) {
@@ -342,7 +353,9 @@ extern "C" int tf_plan_create(int64_t n_dof, int64_t n_elem, const int64_t* elem
           const int32_t len = c == 0 ? len0 : len1;
           for (int32_t a = 0; a < len; a++) lv.maps[ioff + (size_t)c * fm[i] + fwd[a]] = a;
         }
-        const int32_t kp = (fk[i] + 3) & ~3;
+        // panel row stride: k rounded up to kp_align (2: rows stay 16-byte
+        // aligned for cp.async / vector loads; TFB_KP_ALIGN=4 is the round-1 layout)
+        const int32_t kp = (fk[i] + kp_align() - 1) / kp_align() * kp_align();
         // scatter table for the shared-memory front kernels (small fronts)
         int32_t soff = -1;
         if (fm[i] <= kScatterMaxM) {

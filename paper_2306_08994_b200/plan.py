@@ -51,7 +51,7 @@ class LevelTables:
         return np.bincount(self.pattern_of, minlength=self.n_patterns)
 
 
-PLAN_CACHE_VERSION = 1
+PLAN_CACHE_VERSION = 2
 _SCALARS = ("n_dof", "n_leaves", "n_nodes", "n_pivots", "n_levels", "max_m", "max_k")
 _LEVEL_FIELDS = ("level", "n_fronts", "node_base", "piv_base", "n_pivots", "max_m", "max_k",
                  "max_upd")
@@ -62,7 +62,8 @@ def plan_cache_path(fronts: FrontSet, n_dof: int, cache_dir) -> Path:
     """Cache file of the plan of these leaf fronts: keyed by a digest of n_dof, the
     front index lists (in order) and the cache format version."""
     h = hashlib.sha256()
-    h.update(f"tfb-plan-v{PLAN_CACHE_VERSION}:{int(n_dof)}:{len(fronts)}".encode())
+    kp_align = os.environ.get("TFB_KP_ALIGN", "2")  # panel layout knob of the native planner
+    h.update(f"tfb-plan-v{PLAN_CACHE_VERSION}:{kp_align}:{int(n_dof)}:{len(fronts)}".encode())
     h.update(np.ascontiguousarray(fronts.dofs, dtype=np.int32).tobytes())
     if fronts.ptr is not None:
         h.update(np.ascontiguousarray(fronts.ptr, dtype=np.int64).tobytes())
