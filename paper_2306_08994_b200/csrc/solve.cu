@@ -81,8 +81,8 @@ template <int G, int GPC, bool STAGE>
 __global__ void __launch_bounds__(G* GPC)
     solve_fwd_small(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
                     const double* __restrict__ w_child, long long child_rows, int child_at0,
-                    double* w_out, long long out_rows, double* y, int nr, int ldr, int col0,
-                    int smem_per_group) {
+                    double* __restrict__ w_out, long long out_rows, double* __restrict__ y,
+                    int nr, int ldr, int col0, int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   TFB_DIV_SETUP(nr);
@@ -172,6 +172,29 @@ __global__ void __launch_bounds__(G* GPC)
     }
     return;
   }
+  if (!STAGE) {
+    // one column, k <= 4: up to four update rows per thread with all their
+    // panel loads issued before any store
+    for (int r0 = k + t; r0 < m; r0 += 4 * G) {
+      double l[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          l[q][c] = (r0 + q * G < m && c < k) ? __ldg(Pg + (long long)(r0 + q * G) * kp + c) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int r = r0 + q * G;
+        if (r >= m) break;
+        double acc = W[r];
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          if (c < k) acc -= l[q][c] * W[c];
+        out[r - k] = acc;
+      }
+    }
+    return;
+  }
   for (int e = nK + t; e < nW; e += G) {
     const int r = TFB_DIV(e), j = e - r * nr;
     double acc = W[e];
@@ -183,9 +206,9 @@ __global__ void __launch_bounds__(G* GPC)
 template <int G, int GPC, bool STAGE>
 __global__ void __launch_bounds__(G* GPC)
     solve_bwd_small(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
-                    const double* __restrict__ x_parent, long long parent_rows, double* x_out,
-                    long long out_rows, double* y, int nr, int ldr, int col0,
-                    int smem_per_group) {
+                    const double* __restrict__ x_parent, long long parent_rows,
+                    double* __restrict__ x_out, long long out_rows, double* __restrict__ y,
+                    int nr, int ldr, int col0, int smem_per_group) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   TFB_DIV_SETUP(nr);
