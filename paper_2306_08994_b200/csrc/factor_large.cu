@@ -22,6 +22,9 @@
 namespace tfb {
 
 constexpr int NB = 64;  // diagonal block width
+#ifndef TFB_GEMM_MINB
+#define TFB_GEMM_MINB 4  // CTAs per SM the DMMA GEMM kernels are compiled for
+#endif
 
 // Optional per-phase clock stamps of CTA 0 (tools/diag_bench.cu builds with it).
 #ifdef TFB_PHASE_CLOCK
@@ -555,7 +558,7 @@ struct GemmCfg {
 };
 
 template <int MODE, class G>
-__global__ void __launch_bounds__(G::NT, 4) large_update_kernel(LevelArgs L, double* factors,
+__global__ void __launch_bounds__(G::NT, TFB_GEMM_MINB) large_update_kernel(LevelArgs L, double* factors,
                                                             double* upd, int row0, int col0,
                                                             int col1, int t0, int t1,
                                                             const double* __restrict__ child_upd,
