@@ -275,6 +275,12 @@ const char* tf_timing_class_name(int32_t cls);
 /* Library build identification (arch, compile flags). */
 const char* tf_build_info(void);
 
+/* 1 when this level's forward (fwd != 0) or backward sweep for nrhs columns
+ * runs the cooperative wavefront kernels (their whole grid must be
+ * co-resident), 0 otherwise.  Callers overlapping the forward sweep with the
+ * factorization of later levels keep cooperative sweeps after it. */
+int32_t tf_level_solve_cooperative(const tf_level_view* lv, int32_t nrhs, int32_t fwd);
+
 /* Test hook (race detection without compute-sanitizer): seed != 0 makes the
  * CTAs of the flag-synchronised kernels (root dataflow, wavefront sweeps)
  * sleep pseudo-random times at each work item and after each acquire; 0

@@ -37,6 +37,7 @@ from .engine import (
     ExecState,
     FactorResult,
     compile_execution,
+    factor_and_solve,
     factorize,
     init_state,
     run_concurrent,

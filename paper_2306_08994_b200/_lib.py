@@ -75,7 +75,7 @@ EXPORTS = (
     "tf_level_aux_doubles", "tf_level_solve_workspace", "tf_subtree_fusable",
     "tf_subtree_factor", "tf_timing_enable", "tf_timing_collect", "tf_timing_class_name",
     "tf_build_info", "tf_atomic_fnf", "tf_mesh_tensor_device_workspace",
-    "tf_mesh_tensor_device", "tf_mesh_element_values_device",
+    "tf_mesh_tensor_device", "tf_mesh_element_values_device", "tf_level_solve_cooperative",
 )
 
 _lib = None
@@ -137,6 +137,8 @@ def load() -> C.CDLL:
     lib.tf_mesh_tensor_device.restype = C.c_int
     lib.tf_mesh_element_values_device.argtypes = [i32, C.POINTER(i64), i32, vp, vp, vp, vp, vp, vp]
     lib.tf_mesh_element_values_device.restype = C.c_int
+    lib.tf_level_solve_cooperative.argtypes = [C.POINTER(LevelView), i32, i32]
+    lib.tf_level_solve_cooperative.restype = i32
     lib.tf_set_jitter.argtypes = [C.c_uint32]
     lib.tf_set_jitter.restype = C.c_int
     lib.tf_set_small_max_m.argtypes = [i32]

@@ -29,6 +29,7 @@ cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* 
                                   unsigned long long* err, cudaStream_t st);
 int large_level_launches(int max_k, int max_upd, long long level_fronts);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
+int solve_cooperative(const LevelArgs& L, int nrhs, bool fwd);
 cudaError_t set_jitter_solve(unsigned seed);
 cudaError_t set_jitter_factor(unsigned seed);
 int g_small_max_m = 112;  // measured best split on B200 (tools/sweep.sh)
@@ -165,4 +166,9 @@ extern "C" int tf_set_jitter(uint32_t seed) {
   cudaError_t e = set_jitter_factor(seed);
   if (e == cudaSuccess) e = set_jitter_solve(seed);
   return status(e);
+}
+
+extern "C" int32_t tf_level_solve_cooperative(const tf_level_view* lv, int32_t nrhs, int32_t fwd) {
+  if (!lv || lv->n_fronts == 0 || nrhs < 1) return 0;
+  return solve_cooperative(make_args(lv), nrhs, fwd != 0);
 }

@@ -2135,6 +2135,14 @@ cudaError_t launch_solve_bwd(const LevelArgs& L, const LevelArgs& PA, int has_pa
   return cudaGetLastError();
 }
 
+// Whether the level's sweep uses the cooperative wavefront kernels (the
+// caller then keeps it off streams that run concurrently with other kernels).
+int solve_cooperative(const LevelArgs& L, int nrhs, bool fwd) {
+  if (!level_is_large(L.is_leaf, L.max_m)) return 0;
+  if (narrow_solve(L, nrhs) || front_solve(L, nrhs, fwd) || split_solve(L, nrhs, fwd)) return 0;
+  return L.max_k > 0 ? 1 : 0;
+}
+
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   if (cols_solve_fwd(L, nrhs)) return (nrhs + 63) / 64;
   if (!level_is_large(L.is_leaf, L.max_m))

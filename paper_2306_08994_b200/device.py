@@ -212,6 +212,8 @@ class DevicePlan:
         self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
         self._solve_nrhs = 0
         self._blk = None
+        self._side = None     # second stream of factor_solve (overlapped forward sweep)
+        self._lvl_ev = None
         self._fgraph = None   # (threshold, CUDA graph) of factor() (public API path)
         self._sgraphs = {}    # rhs shape -> (graph, static b, static x) of solve_into()
         self.fuse_bottom = True  # run the lowest levels as one subtree kernel when possible
@@ -300,51 +302,99 @@ class DevicePlan:
             self._solve_nrhs = nrhs
         return self._blk
 
-    def solve_into(self, b: torch.Tensor, x: torch.Tensor,
-                   stream: Optional[torch.cuda.Stream] = None) -> None:
-        """x = A^-1 b for row-major (n, nrhs) device tensors (b may alias x)."""
+    def _solve_begin(self, b: torch.Tensor, x: torch.Tensor, sp) -> int:
         nrhs = 1 if b.dim() == 1 else b.shape[1]
-        st = stream or torch.cuda.current_stream(self.device)
-        sp = C.c_void_p(st.cuda_stream)
-        lib = self.lib
         blk = self._blocks(nrhs)
-        y = self._y
         if GUARD:
-            poison(*blk, y)  # (the workspace's flags must start at zero: not poisoned)
-        npiv = self.n_pivots
+            poison(*blk, self._y)  # (the workspace's flags must start at zero: not poisoned)
         if x.data_ptr() != b.data_ptr():
             x.copy_(b)  # DOFs outside every front stay as given (engine.py:481)
-        _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(x), _ptr(y), nrhs, 0,
-                                       sp), "tf_permute_rows")
-        prev = None
-        for L, dl in enumerate(self.levels):
-            cur = blk[L & 1]
-            child = self.levels[L - 1] if L > 0 else None
-            rc = lib.tf_level_solve_fwd(C.byref(dl.view),
-                                        C.byref(child.view) if child else None,
-                                        _ptr(self.factors[L]), _ptr(prev),
-                                        child.max_m if child else 0, _ptr(cur), dl.max_m,
-                                        _ptr(y), nrhs, _ptr(self._ws), self._ws_bytes, sp)
-            _lib.check(rc, f"tf_level_solve_fwd(level {L})")
-            prev = cur
-        prev = None
+        _lib.check(self.lib.tf_permute_rows(_ptr(self.pivot_order), self.n_pivots, _ptr(x),
+                                            _ptr(self._y), nrhs, 0, sp), "tf_permute_rows")
+        return nrhs
+
+    def _solve_fwd_level(self, L: int, nrhs: int, sp) -> None:
+        dl = self.levels[L]
+        blk = self._blk
+        child = self.levels[L - 1] if L > 0 else None
+        rc = self.lib.tf_level_solve_fwd(C.byref(dl.view), C.byref(child.view) if child else None,
+                                         _ptr(self.factors[L]), _ptr(blk[(L - 1) & 1]) if L else None,
+                                         child.max_m if child else 0, _ptr(blk[L & 1]), dl.max_m,
+                                         _ptr(self._y), nrhs, _ptr(self._ws), self._ws_bytes, sp)
+        _lib.check(rc, f"tf_level_solve_fwd(level {L})")
+
+    def _solve_end(self, x: torch.Tensor, nrhs: int, sp) -> None:
+        """Backward sweep (root -> leaves) and the scatter back to natural order."""
+        blk = self._blk
         nl = len(self.levels)
         for L in range(nl - 1, -1, -1):
             dl = self.levels[L]
-            cur = blk[L & 1]
             parent = self.levels[L + 1] if L + 1 < nl else None
-            rc = lib.tf_level_solve_bwd(C.byref(dl.view),
-                                        C.byref(parent.view) if parent else None,
-                                        _ptr(self.factors[L]), _ptr(prev),
-                                        parent.max_m if parent else 0, _ptr(cur), dl.max_m,
-                                        _ptr(y), nrhs, _ptr(self._ws), self._ws_bytes, sp)
+            rc = self.lib.tf_level_solve_bwd(C.byref(dl.view),
+                                             C.byref(parent.view) if parent else None,
+                                             _ptr(self.factors[L]),
+                                             _ptr(blk[(L + 1) & 1]) if parent else None,
+                                             parent.max_m if parent else 0, _ptr(blk[L & 1]),
+                                             dl.max_m, _ptr(self._y), nrhs, _ptr(self._ws),
+                                             self._ws_bytes, sp)
             _lib.check(rc, f"tf_level_solve_bwd(level {L})")
-            prev = cur
-        _lib.check(lib.tf_permute_rows(_ptr(self.pivot_order), npiv, _ptr(y), _ptr(x), nrhs, 1,
-                                       sp), "tf_permute_rows")
+        _lib.check(self.lib.tf_permute_rows(_ptr(self.pivot_order), self.n_pivots, _ptr(self._y),
+                                            _ptr(x), nrhs, 1, sp), "tf_permute_rows")
+
+    def solve_into(self, b: torch.Tensor, x: torch.Tensor,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+        """x = A^-1 b for row-major (n, nrhs) device tensors (b may alias x)."""
+        st = stream or torch.cuda.current_stream(self.device)
+        sp = C.c_void_p(st.cuda_stream)
+        nrhs = self._solve_begin(b, x, sp)
+        for L in range(len(self.levels)):
+            self._solve_fwd_level(L, nrhs, sp)
+        self._solve_end(x, nrhs, sp)
+
+    def factor_solve(self, threshold: float, b: torch.Tensor, x: torch.Tensor,
+                     stream: Optional[torch.cuda.Stream] = None) -> None:
+        """factor(threshold) then x = A^-1 b, with the forward sweep overlapped.
+
+        The forward sweep of level L needs only the factors of levels <= L, so
+        it runs on a second stream right after level L is factored, while the
+        factorization of the levels above proceeds (compute-bound Schur GEMMs
+        next to memory-bound sweeps).  Sweeps that use the cooperative
+        wavefront kernels (tf_level_solve_cooperative) wait for the whole
+        factorization, as does the backward sweep.  Same kernels and order
+        per stream as factor() + solve_into(): identical results."""
+        st = stream or torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+            self._lvl_ev = [torch.cuda.Event() for _ in self.levels]
+        ss = self._side
+        ssp = C.c_void_p(ss.cuda_stream)
+        nrhs = 1 if b.dim() == 1 else b.shape[1]
+        self._blocks(nrhs)
+        ss.wait_stream(st)                       # b (and everything before) ready
+        with torch.cuda.stream(ss):
+            self._solve_begin(b, x, ssp)
+        state = {"next": 0, "open": True}
+
+        def hook(L):
+            self._lvl_ev[L].record(st)
+            while state["open"] and state["next"] <= L:
+                n = state["next"]
+                if self.lib.tf_level_solve_cooperative(C.byref(self.levels[n].view), nrhs, 1):
+                    state["open"] = False
+                    break
+                ss.wait_event(self._lvl_ev[n])
+                self._solve_fwd_level(n, nrhs, ssp)
+                state["next"] = n + 1
+
+        self.factor(threshold, st, level_hook=hook)
+        ss.wait_stream(st)
+        for L in range(state["next"], len(self.levels)):
+            self._solve_fwd_level(L, nrhs, ssp)
+        self._solve_end(x, nrhs, ssp)
+        st.wait_stream(ss)
 
     def capture(self, threshold: float, b: torch.Tensor, x: torch.Tensor,
-                warmup: bool = True) -> "torch.cuda.CUDAGraph":
+                warmup: bool = True, overlap: bool = False) -> "torch.cuda.CUDAGraph":
         """One CUDA graph of a whole factorization + solve (every level's
         launches, the lookahead streams' fork/join, the wavefront sweeps).
 
@@ -357,15 +407,21 @@ class DevicePlan:
         stream = torch.cuda.Stream(self.device)
         stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(stream):
-            if warmup:  # first calls create streams, set kernel attributes, size workspaces
-                self.factor(threshold, stream)
-                self.solve_into(b, x, stream)
+            if warmup or overlap:  # first calls create streams, kernel attributes, workspaces
+                if overlap:
+                    self.factor_solve(threshold, b, x, stream)
+                else:
+                    self.factor(threshold, stream)
+                    self.solve_into(b, x, stream)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             st = torch.cuda.current_stream(self.device)
-            self.factor(threshold, st)
-            self.solve_into(b, x, st)
+            if overlap:  # forward sweep overlapped with the factorization (factor_solve)
+                self.factor_solve(threshold, b, x, st)
+            else:
+                self.factor(threshold, st)
+                self.solve_into(b, x, st)
         torch.cuda.current_stream(self.device).wait_stream(stream)
         return g
 
@@ -409,6 +465,25 @@ class DevicePlan:
             self.solve_into(gb, gx)
             g = self._capture(lambda st: self.solve_into(gb, gx, st))
             self._sgraphs[shape] = (g, gb, gx)
+            x.copy_(gx)
+            return
+        g, gb, gx = ent
+        gb.copy_(b)
+        g.replay()
+        x.copy_(gx)
+
+    def factor_solve_graphed(self, threshold: float, b: torch.Tensor, x: torch.Tensor) -> None:
+        """factor_solve() through a cached graph per (threshold, rhs shape)."""
+        if not USE_GRAPHS or GUARD:
+            return self.factor_solve(threshold, b, x)
+        key = (threshold, tuple(b.shape))
+        ent = self._sgraphs.get(key)
+        if ent is None:
+            gb, gx = torch.empty_like(b), torch.empty_like(b)
+            gb.copy_(b)
+            self.factor_solve(threshold, gb, gx)
+            g = self._capture(lambda st: self.factor_solve(threshold, gb, gx, st))
+            self._sgraphs[key] = (g, gb, gx)
             x.copy_(gx)
             return
         g, gb, gx = ent

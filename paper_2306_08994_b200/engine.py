@@ -306,6 +306,30 @@ def run_concurrent(schedule, plan, state: ExecState, workers: int = 1, debug: bo
     return res
 
 
+def factor_and_solve(plan, state: ExecState, rhs, compiled: Optional[DevicePlan] = None):
+    """run_sequential(plan, state) + solve(factors, rhs) in one call, with the
+    forward sweep of each level overlapped with the factorization of the levels
+    above it (DevicePlan.factor_solve; same results).  Returns (factors, x);
+    x has rhs's kind and shape.  Raises ZeroPivotError like run_sequential."""
+    plan = _plan_of(plan)
+    dp = compiled or state.compiled or compile_execution(plan, None, state)
+    n = plan.n_dof
+    if not isinstance(rhs, torch.Tensor):
+        arr = np.asarray(rhs, dtype=float)
+        if arr.shape[:1] != (n,) or arr.ndim > 2:
+            raise ValueError(f"rhs must have length {n}, got {arr.shape}")
+    b = _as_device(rhs, dp.device, n)
+    x = torch.empty_like(b)
+    dp.factor_solve_graphed(state.zero_threshold, b, x)
+    pos = dp.zero_pivot_position()
+    if pos >= 0:
+        front, pivot = plan.locate_pivot(pos)
+        raise ZeroPivotError(front, pivot)
+    res = FactorResult(plan, dp)
+    state.factors = res
+    return res, (x if isinstance(rhs, torch.Tensor) else x.cpu().numpy())
+
+
 def factorize(plan, system) -> FactorResult:
     """Convenience: init_state + run_sequential."""
     return run_sequential(plan, init_state(system, plan))
