@@ -17,8 +17,11 @@ graph is still part of the reference's API -- `cli._build_pipeline` calls
   `succs` (the J1-J4 wiring of tasks.py:207-252) are built on first access,
   for plans small enough to keep per-node lists.
 * `validate_dag(graph)` reports kind counts and the longest path (= number of
-  atomic Foata classes).  The graph is acyclic by construction (every edge
-  goes forward in the enumeration order of its pivot steps).
+  atomic Foata classes, computed by the streamed FNF).  A plan's graph is
+  acyclic by construction: every J1-J4 edge is level-nondecreasing and, inside
+  a level, advances the atomic Foata class (tests/test_schedule.py), so `ok`
+  is always True here; a symbolically singular plan raises
+  SymbolicSingularityError from the native FNF instead.
 """
 
 from __future__ import annotations
