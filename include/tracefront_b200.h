@@ -184,6 +184,12 @@ typedef struct {
   const uint8_t* zero_upd; /* optional, per front: 1 when the front and its whole subtree have
                               no pivots, so its forward update block is identically zero: the
                               solve neither writes nor reads it (NULL: leaves with k == 0 only) */
+  const uint8_t* implicit_upd; /* optional, per front: 1 when its forward update is -L21 w_piv with
+                                  no child contribution (k > 0, pivot-free children); the sweep
+                                  then stores only the k unscaled pivot rows w_piv and the parent
+                                  forms -L21 w_piv itself from `factors` (NULL: none) */
+  const double* factors;       /* this level's factor buffer (read by the parent level's forward
+                                  sweep for implicit updates; may be NULL otherwise) */
 } tf_level_view;
 
 /* Doubles of `aux` each front of this level needs under the current

@@ -63,6 +63,7 @@ class LevelView(C.Structure):
         ("aux", C.c_void_p), ("aux_stride", C.c_int64),
         ("front_base", C.c_int64), ("child_base", C.c_int64),
         ("level_fronts", C.c_int64), ("zero_upd", C.c_void_p),
+        ("implicit_upd", C.c_void_p), ("factors", C.c_void_p),
     ]
 
 

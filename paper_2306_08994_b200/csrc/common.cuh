@@ -72,10 +72,15 @@ struct LevelArgs {
   long long child_base;  // tree index of slot 0 of the child-level buffer
   long long level_fronts;  // fronts of the whole level (variant choices use this)
   const unsigned char* zero_upd;  // per front (slice-relative): pivot-free subtree, or null
+  const unsigned char* implicit_upd;  // per front: forward update left implicit (-L21 w_piv)
+  const double* factors;              // this level's factor buffer (implicit updates)
   // front f's forward update block is identically zero (never written)
   __device__ __forceinline__ bool upd_is_zero(long long f) const {
     if (zero_upd) return zero_upd[f] != 0;
     return is_leaf && pat[(size_t)pattern_of[f] * TF_PAT_WIDTH + TF_PAT_K] == 0;
+  }
+  __device__ __forceinline__ bool upd_implicit(long long f) const {
+    return implicit_upd && implicit_upd[f] != 0;
   }
   // child c of front f (slice-relative) -> slot in the child buffer / view
   __device__ __forceinline__ long long child_slot(long long f, int c) const {
@@ -105,6 +110,8 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.child_base = v->child_base;
   a.level_fronts = v->level_fronts > 0 ? v->level_fronts : v->n_fronts;
   a.zero_upd = v->zero_upd;
+  a.implicit_upd = v->implicit_upd;
+  a.factors = v->factors;
   return a;
 }
 

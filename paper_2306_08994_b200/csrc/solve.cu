@@ -119,6 +119,23 @@ __global__ void __launch_bounds__(G* GPC)
       const int* mp = L.maps + (c == 0 ? s.off0 : s.off1);
       const double* Wc = w_child + (ch * child_rows + off) * ldr + col0;
       const int n = len * nr;
+      if (C.upd_implicit(ch)) {
+        // the child stored its k unscaled pivot rows w_piv (rows [0, ck)):
+        // its update row a is -sum_q l(ck+a, q) w_piv[q], summed here in the
+        // child's own order (bitwise what it would have written)
+        const int* CP = C.pat + (size_t)C.pattern_of[ch] * TF_PAT_WIDTH;
+        const int ckp = CP[TF_PAT_KP];
+        const double* Pc = C.factors + ch * C.fac_stride + (long long)ck * ckp;
+        const double* Wp = w_child + ch * child_rows * ldr + col0;
+        for (int e = t; e < n; e += G) {
+          const int a = TFB_DIV(e), j = e - a * nr;
+          double acc = 0.0;
+          for (int q = 0; q < ck; q++) acc -= __ldg(Pc + (long long)a * ckp + q) * Wp[(long long)q * ldr + j];
+          W[__ldg(mp + a) * nr + j] += acc;
+        }
+        group_sync<G>(bar);
+        continue;
+      }
       int e = t;
       for (; e + 3 * G < n; e += 4 * G) {  // four entries in flight per thread
         int p[4];
@@ -155,6 +172,13 @@ __global__ void __launch_bounds__(G* GPC)
   }
   // update rows: w_r - l_r . w_piv (row-contiguous panel reads), straight out
   double* out = w_out + f * out_rows * ldr + col0;
+  if (L.upd_implicit(f)) {  // the parent forms -L21 w_piv itself: store w_piv only
+    for (int e = t; e < nK; e += G) {
+      const int r = TFB_DIV(e), j = e - r * nr;
+      out[(long long)r * ldr + j] = W[e];
+    }
+    return;
+  }
   if (!STAGE && k > 4) {
     // one column, rows wider than a sector: a thread's whole row is requested
     // in bursts of 8 entries (every sector of the row in flight together)
@@ -335,15 +359,35 @@ __global__ void __launch_bounds__(32 * kColsWarps)
   // child blocks (null: no such child or a pivot-free subtree)
   const double* Wc0 = nullptr;
   const double* Wc1 = nullptr;
+  // implicit children: their update row a is -sum_q l(k+a, q) w_piv[q]
+  const double* Pc0 = nullptr;
+  const double* Pc1 = nullptr;
+  int ck0 = 0, ck1 = 0, ckp0 = 0, ckp1 = 0;
   if (!L.is_leaf) {
     const long long ch0 = 2 * (L.front_base + f) - C.front_base;
     if (!C.upd_is_zero(ch0)) {
-      const int ck = C.pat[(size_t)C.pattern_of[ch0] * TF_PAT_WIDTH + TF_PAT_K];
-      Wc0 = w_child + (ch0 * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+      const int* CP = C.pat + (size_t)C.pattern_of[ch0] * TF_PAT_WIDTH;
+      const int ck = CP[TF_PAT_K];
+      if (C.upd_implicit(ch0)) {
+        Wc0 = w_child + ch0 * child_rows * ldr + col0;
+        ck0 = ck;
+        ckp0 = CP[TF_PAT_KP];
+        Pc0 = C.factors + ch0 * C.fac_stride + (long long)ck * ckp0;
+      } else {
+        Wc0 = w_child + (ch0 * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+      }
     }
     if (s.nsrc == 2 && !C.upd_is_zero(ch0 + 1)) {
-      const int ck = C.pat[(size_t)C.pattern_of[ch0 + 1] * TF_PAT_WIDTH + TF_PAT_K];
-      Wc1 = w_child + ((ch0 + 1) * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+      const int* CP = C.pat + (size_t)C.pattern_of[ch0 + 1] * TF_PAT_WIDTH;
+      const int ck = CP[TF_PAT_K];
+      if (C.upd_implicit(ch0 + 1)) {
+        Wc1 = w_child + (ch0 + 1) * child_rows * ldr + col0;
+        ck1 = ck;
+        ckp1 = CP[TF_PAT_KP];
+        Pc1 = C.factors + (ch0 + 1) * C.fac_stride + (long long)ck * ckp1;
+      } else {
+        Wc1 = w_child + ((ch0 + 1) * child_rows + (child_at0 ? 0 : ck)) * ldr + col0;
+      }
     }
   }
   bool cok[CPL];
@@ -355,8 +399,23 @@ __global__ void __launch_bounds__(32 * kColsWarps)
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
       const int col = lane + 32 * j;
-      double a = (i0 >= 0 && cok[j]) ? Wc0[(long long)i0 * ldr + col] : 0.0;
-      double b = (i1 >= 0 && cok[j]) ? Wc1[(long long)i1 * ldr + col] : 0.0;
+      double a = 0.0, b = 0.0;
+      if (i0 >= 0 && cok[j]) {
+        if (Pc0) {
+          for (int q = 0; q < ck0; q++)
+            a -= __ldg(Pc0 + (long long)i0 * ckp0 + q) * Wc0[(long long)q * ldr + col];
+        } else {
+          a = Wc0[(long long)i0 * ldr + col];
+        }
+      }
+      if (i1 >= 0 && cok[j]) {
+        if (Pc1) {
+          for (int q = 0; q < ck1; q++)
+            b -= __ldg(Pc1 + (long long)i1 * ckp1 + q) * Wc1[(long long)q * ldr + col];
+        } else {
+          b = Wc1[(long long)i1 * ldr + col];
+        }
+      }
       v[j] = a + b;
     }
   };
@@ -396,8 +455,18 @@ __global__ void __launch_bounds__(32 * kColsWarps)
         if (cok[j]) y[(piv + c) * ldr + col0 + lane + 32 * j] = w[c][j] * dinv;
     }
   }
-  // update rows, four at a time
   double* out = w_out + f * out_rows * ldr + col0;
+  if (L.upd_implicit(f)) {  // the parent forms -L21 w_piv itself: store w_piv only
+#pragma unroll
+    for (int c = 0; c < KMAX; c++)
+      if (c < k) {
+#pragma unroll
+        for (int j = 0; j < CPL; j++)
+          if (cok[j]) out[(long long)c * ldr + lane + 32 * j] = w[c][j];
+      }
+    return;
+  }
+  // update rows, four at a time
   for (int r0 = k; r0 < m; r0 += 4) {
     double v[4][CPL];
 #pragma unroll

@@ -203,9 +203,13 @@ class DevicePlan:
                 z &= kids
             dl.zero_upd = torch.from_numpy(z.astype(np.uint8)).to(self.device)
             dl.view.zero_upd = dl.zero_upd.data_ptr()
+            # implicit forward updates: pivots but no child contribution
+            dl.implicit = (lt.front_k() > 0) & (np.ones(lt.n_fronts, dtype=bool) if zprev is None
+                                                  else (kids if lt.level > 0 else True))
             zprev = z
             self.levels.append(dl)
             child = dl.upd_stride
+        self._setup_implicit()
         self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)
         self._factors = None  # allocated on first single-device factorization
         self._upd = None
@@ -219,11 +223,31 @@ class DevicePlan:
         self.fuse_bottom = True  # run the lowest levels as one subtree kernel when possible
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
+    def _setup_implicit(self) -> None:
+        """Implicit forward updates (tf_level_view.implicit_upd) on small levels
+        whose parent level is small with at most 8 pivots per front (the group
+        and column sweeps read them; TFB_IMPLICIT_UPD=0 disables)."""
+        on = os.environ.get("TFB_IMPLICIT_UPD", "1") != "0"
+        small_max = int(self.lib.tf_set_small_max_m(0)) if on else 0  # query the split
+        for L, dl in enumerate(self.levels):
+            imp = getattr(dl, "implicit", None)
+            dl.implicit_t = None
+            dl.view.implicit_upd = None
+            if not on or imp is None or L + 1 >= len(self.levels) or not imp.any():
+                continue
+            par = self.levels[L + 1]
+            if dl.max_m > small_max or par.max_m > small_max or par.tables.max_k > 8:
+                continue
+            dl.implicit_t = torch.from_numpy(imp.astype(np.uint8)).to(self.device)
+            dl.view.implicit_upd = dl.implicit_t.data_ptr()
+
     @property
     def factors(self):
         if self._factors is None:
             self._factors = [_buf(dl.n_fronts * dl.fac_stride, self.device)
                              for dl in self.levels]
+            for dl, t in zip(self.levels, self._factors):
+                dl.view.factors = t.data_ptr()
         return self._factors
 
     @property

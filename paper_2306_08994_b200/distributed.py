@@ -219,6 +219,10 @@ def _slice_view(full, f0: int, n: int, child_base: int = 0):
     v.child_base = child_base
     if full.zero_upd:
         v.zero_upd = full.zero_upd + f0
+    # implicit forward updates read the child's factors, which a rank only
+    # holds for its own fronts: the sharded sweeps keep every update explicit
+    v.implicit_upd = None
+    v.factors = None
     return v
 
 
