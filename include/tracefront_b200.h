@@ -190,6 +190,16 @@ typedef struct {
                                   forms -L21 w_piv itself from `factors` (NULL: none) */
   const double* factors;       /* this level's factor buffer (read by the parent level's forward
                                   sweep for implicit updates; may be NULL otherwise) */
+  int32_t leaf_direct; /* optional leaf pass-through (0: off).  Leaf level: fronts without
+                          pivots write no update (it is their element matrix in front order).
+                          Level 1 (shared-memory fronts only): such a leaf child is read from
+                          its element matrix (elem, elem_stride of this view) instead of the
+                          child-update buffer, through the tables below. */
+  const int32_t* src_pattern_of; /* level 1 with leaf_direct: the leaf level's pattern_of */
+  const int32_t* src_pat;        /* and pat; */
+  const int32_t* src_maps;       /* per leaf pattern p: src_maps[p] = offset in src_maps of the
+                                    table e -> element index (row-major, lower part) of entry e
+                                    of the leaf's packed update */
 } tf_level_view;
 
 /* Doubles of `aux` each front of this level needs under the current

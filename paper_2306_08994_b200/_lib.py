@@ -64,6 +64,8 @@ class LevelView(C.Structure):
         ("front_base", C.c_int64), ("child_base", C.c_int64),
         ("level_fronts", C.c_int64), ("zero_upd", C.c_void_p),
         ("implicit_upd", C.c_void_p), ("factors", C.c_void_p),
+        ("leaf_direct", C.c_int32), ("src_pattern_of", C.c_void_p),
+        ("src_pat", C.c_void_p), ("src_maps", C.c_void_p),
     ]
 
 

@@ -71,8 +71,12 @@ extern "C" int tf_level_factor(const tf_level_view* lv, const double* child_upd,
   if (!lv->is_leaf && !child_upd) return TF_ERR_INVALID;
   LevelArgs L = make_args(lv);
   cudaStream_t st = (cudaStream_t)stream;
+  if (lv->leaf_direct && !lv->is_leaf && (!elem || !lv->src_pattern_of || !lv->src_pat ||
+                                          !lv->src_maps || lv->front_base != 0))
+    return TF_ERR_INVALID;
   if (!level_is_large(lv->is_leaf, lv->max_m))
     return status(launch_factor_small(L, child_upd, elem, factors, upd_out, threshold, err, st));
+  if (lv->leaf_direct) return TF_ERR_INVALID;  // pass-through leaves need the shared-memory path
   if (lv->max_k > 0 && (!lv->aux || lv->aux_stride < large_aux_doubles(lv->max_k)))
     return TF_ERR_INVALID;
   int* flags = nullptr;
@@ -98,6 +102,7 @@ extern "C" int tf_subtree_factor(const tf_level_view* views, int32_t nlev,
   LevelArgs lv[10];
   for (int L = 0; L < nlev; L++) {
     lv[L] = make_args(&views[L]);
+    lv[L].leaf_direct = 0;  // the subtree kernel keeps every update in shared memory
     if (level_is_large(lv[L].is_leaf, lv[L].max_m) || lv[L].front_base != 0) return TF_ERR_INVALID;
   }
   return status(launch_factor_subtree(lv, nlev, factors, elem, upd_out, threshold, err,

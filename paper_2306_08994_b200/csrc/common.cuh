@@ -74,6 +74,10 @@ struct LevelArgs {
   const unsigned char* zero_upd;  // per front (slice-relative): pivot-free subtree, or null
   const unsigned char* implicit_upd;  // per front: forward update left implicit (-L21 w_piv)
   const double* factors;              // this level's factor buffer (implicit updates)
+  int leaf_direct;                    // leaf pass-through (tf_level_view.leaf_direct)
+  const int* __restrict__ src_pattern_of;  // level 1 with leaf_direct: leaf-level tables
+  const int* __restrict__ src_pat;
+  const int* __restrict__ src_maps;
   // front f's forward update block is identically zero (never written)
   __device__ __forceinline__ bool upd_is_zero(long long f) const {
     if (zero_upd) return zero_upd[f] != 0;
@@ -112,6 +116,10 @@ inline LevelArgs make_args(const tf_level_view* v) {
   a.zero_upd = v->zero_upd;
   a.implicit_upd = v->implicit_upd;
   a.factors = v->factors;
+  a.leaf_direct = v->leaf_direct;
+  a.src_pattern_of = v->src_pattern_of;
+  a.src_pat = v->src_pat;
+  a.src_maps = v->src_maps;
   return a;
 }
 

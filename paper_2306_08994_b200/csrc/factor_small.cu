@@ -50,18 +50,28 @@ __device__ __forceinline__ void chunk_of(int n, int G, int t, int& beg, int& end
   end = min(n, beg + c);
 }
 
+// Pivots of leaf child c of level-1 front f (leaf pass-through, leaf_direct).
+__device__ __forceinline__ int leaf_child_k(const LevelArgs& L, long long f, int c) {
+  const long long ch = L.child_slot(f, c);
+  return L.src_pat[(size_t)L.src_pattern_of[ch] * TF_PAT_WIDTH + TF_PAT_K];
+}
+
 // One front, one thread group: extend-add of src0/src1 (packed child Schur
 // blocks, or the element matrix at the leaves), partial LDL^T, Schur block,
 // copy-out of the factor slot and of the packed update to upd_dst.
 template <int G>
 __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, const Shape& S,
                                              const double* __restrict__ src0,
-                                             const double* __restrict__ src1, double* F,
+                                             const double* __restrict__ src1,
+                                             const double* __restrict__ elem, double* F,
                                              double* lv, double* __restrict__ fac_out,
                                              double* __restrict__ upd_dst, double threshold,
                                              unsigned long long* err, int t, int bar,
                                              int fs_k = 16) {
   const int m = S.m, k = S.k, kp = S.kp, u = m - k;
+  // leaf pass-through: a leaf without pivots writes nothing; level 1 reads its
+  // element matrix instead of its update (tf_level_view.leaf_direct)
+  if (L.is_leaf && L.leaf_direct && k == 0) return;
   const int ks = kp + 1, tk = (int)tri32(k, 0), nS = (int)tri32(u, 0), s0 = tk + u * ks;
   double* Sb = F + s0;
   auto rowp = [&](int r) { return r < k ? (int)tri32(r, 0) : tk + (r - k) * ks; };
@@ -89,6 +99,26 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
           if (++b > a) { a++; b = 0; }
         }
       }
+    } else if (L.leaf_direct && leaf_child_k(L, f, c) == 0) {
+      // pivot-free leaf child: entry e of its update is the element-matrix
+      // entry di[e] (src_maps: per leaf pattern, packed update index ->
+      // element index, lower part) -- exactly what the leaf would have written
+      const long long ch = L.child_slot(f, c);
+      const int* di = L.src_maps + L.src_maps[L.src_pattern_of[ch]];
+      const double* E = elem + ch * L.elem_stride;
+      int e = t;
+      for (; e + 3 * G < n; e += 4 * G) {
+        int p[4];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          p[q] = __ldg(scc + e + q * G);
+          v[q] = E[__ldg(di + e + q * G)];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) F[p[q]] += v[q];
+      }
+      for (; e < n; e += G) F[__ldg(scc + e)] += E[__ldg(di + e)];
     } else {
       const double* src = c == 0 ? src0 : src1;
       int e = t;
@@ -262,17 +292,20 @@ __global__ void __launch_bounds__(G* GPC)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gid = threadIdx.x / G;
   const int t = threadIdx.x - gid * G;
-  const long long f = (long long)blockIdx.x * GPC + gid;
-  if (f >= L.n_fronts) return;  // whole group exits; syncs are group-local
   unsigned char* my = smem_raw + (size_t)gid * smem_per_group;
   double* F = reinterpret_cast<double*>(my);
   double* lv = F + small_front_doubles(L.max_m, L.max_k) - L.max_m;
-  const Shape S = front_shape(L, f);
-  const double* s0 = L.is_leaf ? elem + f * L.elem_stride
-                               : child_upd + L.child_slot(f, 0) * L.child_upd_stride;
-  const double* s1 = L.is_leaf ? nullptr : child_upd + L.child_slot(f, 1) * L.child_upd_stride;
-  factor_front<G>(L, f, S, s0, s1, F, lv, factors + f * L.fac_stride,
-                  upd_out + f * L.upd_stride, threshold, err, t, 1 + gid, fs_k);
+  // grid-stride over fronts (the grid covers the level except on pass-through
+  // leaf levels, where most fronts return at once); syncs are group-local
+  for (long long f = (long long)blockIdx.x * GPC + gid; f < L.n_fronts;
+       f += (long long)gridDim.x * GPC) {
+    const Shape S = front_shape(L, f);
+    const double* s0 = L.is_leaf ? elem + f * L.elem_stride
+                                 : child_upd + L.child_slot(f, 0) * L.child_upd_stride;
+    const double* s1 = L.is_leaf ? nullptr : child_upd + L.child_slot(f, 1) * L.child_upd_stride;
+    factor_front<G>(L, f, S, s0, s1, elem, F, lv, factors + f * L.fac_stride,
+                    upd_out + f * L.upd_stride, threshold, err, t, 1 + gid, fs_k);
+  }
 }
 
 template <int G, int GPC>
@@ -295,8 +328,11 @@ static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, c
     const char* e = getenv("TFB_SMALL_FSK");
     fs_k = e ? atoi(e) : 16;
   }
-  kern<<<(unsigned)blocks, G * GPC, smem, st>>>(L, child_upd, elem, factors, upd_out, thr, err,
-                                                per, fs_k);
+  // pass-through leaves: nearly every front returns at once, so a few resident
+  // waves of CTAs stride over the level instead of one CTA per GPC fronts
+  const long long grid = (L.is_leaf && L.leaf_direct) ? std::min(blocks, 148LL * 16) : blocks;
+  kern<<<(unsigned)grid, G * GPC, smem, st>>>(L, child_upd, elem, factors, upd_out, thr, err,
+                                              per, fs_k);
   timer_end(st);
   return cudaGetLastError();
 }
@@ -380,7 +416,7 @@ __global__ void __launch_bounds__(kSubG* kSubNG) factor_subtree_kernel(
       const double* s0 = lv.is_leaf ? elem + f * lv.elem_stride : prev + (2 * i) * cst;
       const double* s1 = lv.is_leaf ? nullptr : prev + (2 * i + 1) * cst;
       double* dst = L == top ? upd_out + f * lv.upd_stride : cur + i * ost;
-      factor_front<kSubG>(lv, f, S, s0, s1, F, lvec, A.fac[L] + f * lv.fac_stride, dst,
+      factor_front<kSubG>(lv, f, S, s0, s1, elem, F, lvec, A.fac[L] + f * lv.fac_stride, dst,
                           threshold, err, t, 0);
       group_sync<kSubG>(0);
     }

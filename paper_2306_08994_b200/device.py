@@ -210,6 +210,7 @@ class DevicePlan:
             self.levels.append(dl)
             child = dl.upd_stride
         self._setup_implicit()
+        self._setup_leaf_direct()
         self.pivot_order = torch.from_numpy(native.pivot_order).to(self.device)
         self._factors = None  # allocated on first single-device factorization
         self._upd = None
@@ -240,6 +241,43 @@ class DevicePlan:
                 continue
             dl.implicit_t = torch.from_numpy(imp.astype(np.uint8)).to(self.device)
             dl.view.implicit_upd = dl.implicit_t.data_ptr()
+
+    def _setup_leaf_direct(self) -> None:
+        """Leaf pass-through (tf_level_view.leaf_direct): leaves without pivots
+        write no update and level 1 reads their element matrices instead --
+        the leaf level's update round trip through device memory disappears
+        (2D Q1: 99.99% of the leaves).  Needs level 1 on the shared-memory
+        path; TFB_LEAF_DIRECT=0 disables."""
+        on = os.environ.get("TFB_LEAF_DIRECT", "1") != "0"
+        if len(self.levels) < 2:
+            return
+        small_max = int(self.lib.tf_set_small_max_m(0))  # query the split
+        l0, l1 = self.levels[0], self.levels[1]
+        use = on and l1.max_m <= small_max
+        for dl in (l0, l1):
+            dl.view.leaf_direct = 1 if use else 0
+        l1.view.src_pattern_of = l0.view.pattern_of if use else None
+        l1.view.src_pat = l0.view.pat if use else None
+        l1.view.src_maps = None
+        if not use:
+            return
+        # per leaf pattern: entry e = (pa, pb), pa >= pb, of the leaf's packed
+        # update (front order) -> index of its element-matrix entry, lower part
+        # (rows inv[pa], inv[pb] of the element; inv = the pattern's inverse map)
+        lt = l0.tables
+        ld = l0.view.elem_ld
+        tabs, offs, pos = [], [], lt.n_patterns
+        for p in range(lt.n_patterns):
+            m = int(lt.pat[p, _lib.PAT_M])
+            inv = lt.maps[lt.pat[p, _lib.PAT_IOFF]:lt.pat[p, _lib.PAT_IOFF] + m].astype(np.int64)
+            pa, pb = np.tril_indices(m)
+            ra, rb = inv[pa], inv[pb]
+            tabs.append((np.maximum(ra, rb) * ld + np.minimum(ra, rb)).astype(np.int32))
+            offs.append(pos)
+            pos += len(tabs[-1])
+        arr = np.concatenate([np.asarray(offs, np.int32)] + tabs)
+        l1.leaf_index = torch.from_numpy(arr).to(self.device)
+        l1.view.src_maps = l1.leaf_index.data_ptr()
 
     @property
     def factors(self):

@@ -212,6 +212,7 @@ def _slice_view(full, f0: int, n: int, child_base: int = 0):
     """View of fronts [f0, f0+n) of a level; tree relations stay absolute."""
     v = _lib.LevelView()
     C.memmove(C.byref(v), C.byref(full), C.sizeof(_lib.LevelView))
+    v.leaf_direct = 0  # every rank's leaf updates are written (slices read them as usual)
     v.n_fronts = n
     v.pattern_of = (full.pattern_of or 0) + 4 * f0
     v.piv_off = (full.piv_off or 0) + 8 * f0
