@@ -78,21 +78,18 @@ struct PanelRef {
 };
 
 template <int G, int GPC, bool STAGE>
-__global__ void __launch_bounds__(G* GPC)
-    solve_fwd_small(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
-                    const double* __restrict__ w_child, long long child_rows, int child_at0,
-                    double* __restrict__ w_out, long long out_rows, double* __restrict__ y,
-                    int nr, int ldr, int col0, int smem_per_group) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void solve_fwd_small_front(
+    long long f, const LevelArgs& L, const LevelArgs& C, const double* __restrict__ factors,
+    const double* __restrict__ w_child, long long child_rows, int child_at0,
+    double* __restrict__ w_out, long long out_rows, double* __restrict__ y, int nr, int ldr,
+    int col0, int smem_per_group, unsigned char* smem_raw) {
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   TFB_DIV_SETUP(nr);
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
-  const long long f = (long long)blockIdx.x * GPC + gid;
-  if (f >= L.n_fronts) return;
+  if (L.upd_is_zero(f)) return;  // pivot-free subtree: zero update, not written (parent skips it)
   double* W = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  if (L.upd_is_zero(f)) return;  // pivot-free subtree: zero update, not written (parent skips it)
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -228,21 +225,19 @@ __global__ void __launch_bounds__(G* GPC)
 }
 
 template <int G, int GPC, bool STAGE>
-__global__ void __launch_bounds__(G* GPC)
-    solve_bwd_small(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
-                    const double* __restrict__ x_parent, long long parent_rows,
-                    double* __restrict__ x_out, long long out_rows, double* __restrict__ y,
-                    int nr, int ldr, int col0, int smem_per_group) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void solve_bwd_small_front(
+    long long f, const LevelArgs& L, const LevelArgs& PA, int has_parent,
+    const double* __restrict__ factors, const double* __restrict__ x_parent,
+    long long parent_rows, double* __restrict__ x_out, long long out_rows,
+    double* __restrict__ y, int nr, int ldr, int col0, int smem_per_group,
+    unsigned char* smem_raw) {
   if (!STAGE) nr = 1;  // one-column instantiation: index math folds
   TFB_DIV_SETUP(nr);
   const int gid = threadIdx.x / G, t = threadIdx.x - gid * G, bar = 1 + gid;
-  const long long f = (long long)blockIdx.x * GPC + gid;
-  if (f >= L.n_fronts) return;
+  if (L.upd_is_zero(f)) return;  // pivot-free subtree: nothing to solve, no children to serve
   double* X = reinterpret_cast<double*>(smem_raw + (size_t)gid * smem_per_group);
   const Shape s = front_shape(L, f);
   const int m = s.m, k = s.k, kp = s.kp;
-  if (L.upd_is_zero(f)) return;  // pivot-free subtree: nothing to solve, no children to serve
   const long long piv = L.piv_off[f];
   const double* Pg = factors + f * L.fac_stride;
   PanelRef<STAGE> Lp{Pg, kp};
@@ -327,6 +322,36 @@ __global__ void __launch_bounds__(G* GPC)
       out[(long long)r * ldr + j] = X[e];
     }
   }
+}
+
+// Small-front sweep kernels: one thread group per front, grid-stride (leaf
+// levels, whose fronts are nearly all pivot-free and return at once, run on
+// a few resident waves of CTAs; the group-local syncs never span fronts).
+template <int G, int GPC, bool STAGE>
+__global__ void __launch_bounds__(G* GPC)
+    solve_fwd_small(LevelArgs L, LevelArgs C, const double* __restrict__ factors,
+                    const double* __restrict__ w_child, long long child_rows, int child_at0,
+                    double* __restrict__ w_out, long long out_rows, double* __restrict__ y,
+                    int nr, int ldr, int col0, int smem_per_group) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  for (long long f = (long long)blockIdx.x * GPC + threadIdx.x / G; f < L.n_fronts;
+       f += (long long)gridDim.x * GPC)
+    solve_fwd_small_front<G, GPC, STAGE>(f, L, C, factors, w_child, child_rows, child_at0, w_out,
+                                         out_rows, y, nr, ldr, col0, smem_per_group, smem_raw);
+}
+
+template <int G, int GPC, bool STAGE>
+__global__ void __launch_bounds__(G* GPC)
+    solve_bwd_small(LevelArgs L, LevelArgs PA, int has_parent, const double* __restrict__ factors,
+                    const double* __restrict__ x_parent, long long parent_rows,
+                    double* __restrict__ x_out, long long out_rows, double* __restrict__ y,
+                    int nr, int ldr, int col0, int smem_per_group) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  for (long long f = (long long)blockIdx.x * GPC + threadIdx.x / G; f < L.n_fronts;
+       f += (long long)gridDim.x * GPC)
+    solve_bwd_small_front<G, GPC, STAGE>(f, L, PA, has_parent, factors, x_parent, parent_rows,
+                                         x_out, out_rows, y, nr, ldr, col0, smem_per_group,
+                                         smem_raw);
 }
 
 // Many right-hand sides on small levels: one warp per front, lane l owns
@@ -1884,7 +1909,10 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
   const size_t pan = STAGE ? (size_t)L.max_m * L.max_k + L.max_m : 0;
   const int per = (int)(((size_t)L.max_m * nr + pan) * 8 + 15) & ~15;
   const size_t smem = (size_t)per * GPC;
-  const unsigned blocks = (unsigned)((L.n_fronts + GPC - 1) / GPC);
+  const unsigned full = (unsigned)((L.n_fronts + GPC - 1) / GPC);
+  // leaf levels: nearly every front is pivot-free (returns at once): a few
+  // resident waves of CTAs stride over the level
+  const unsigned blocks = L.is_leaf ? std::min(full, 148u * 16u) : full;
   if (FWD) {
     auto kern = solve_fwd_small<G, GPC, STAGE>;
     if (smem > 48 * 1024)
