@@ -181,9 +181,11 @@ typedef struct {
   int64_t child_base; /* tree index of the front held in slot 0 of the child-level buffer */
   int64_t level_fronts; /* fronts of the whole level (a slice keeps the full count, so every
                            rank picks the same kernel variants) */
-  const uint8_t* zero_upd; /* optional, per front: 1 when the front and its whole subtree have
-                              no pivots, so its forward update block is identically zero: the
-                              solve neither writes nor reads it (NULL: leaves with k == 0 only) */
+  const uint8_t* zero_upd; /* optional, per front: bit 0 when the front and its whole subtree
+                              have no pivots, so its forward update block is identically zero:
+                              the solve neither writes nor reads it (NULL: leaves with k == 0
+                              only); bit 1 when every child has such a subtree, so no child reads
+                              the front's backward block (it is not written) */
   const uint8_t* implicit_upd; /* optional, per front: 1 when its forward update is -L21 w_piv with
                                   no child contribution (k > 0, pivot-free children); the sweep
                                   then stores only the k unscaled pivot rows w_piv and the parent

@@ -80,8 +80,13 @@ struct LevelArgs {
   const int* __restrict__ src_maps;
   // front f's forward update block is identically zero (never written)
   __device__ __forceinline__ bool upd_is_zero(long long f) const {
-    if (zero_upd) return zero_upd[f] != 0;
+    if (zero_upd) return (zero_upd[f] & 1) != 0;
     return is_leaf && pat[(size_t)pattern_of[f] * TF_PAT_WIDTH + TF_PAT_K] == 0;
+  }
+  // every child of front f has a pivot-free subtree: no child reads the
+  // front's backward block
+  __device__ __forceinline__ bool children_idle(long long f) const {
+    return zero_upd && (zero_upd[f] & 2) != 0;
   }
   __device__ __forceinline__ bool upd_implicit(long long f) const {
     return implicit_upd && implicit_upd[f] != 0;

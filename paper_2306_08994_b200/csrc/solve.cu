@@ -315,7 +315,7 @@ __device__ __forceinline__ void solve_bwd_small_front(
     const int r = TFB_DIV(e), j = e - r * nr;
     y[(piv + r) * ldr + col0 + j] = X[e];
   }
-  if (!L.is_leaf) {
+  if (!L.is_leaf && !L.children_idle(f)) {  // (children without pivots never read it)
     double* out = x_out + f * out_rows * ldr + col0;
     for (int e = t; e < nW; e += G) {
       const int r = TFB_DIV(e), j = e - r * nr;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(32 * kColsWarps)
 #pragma unroll
     for (int j = 0; j < CPL; j++)
       x[c][j] = (c < k && cok[j]) ? y[(piv + c) * ldr + col0 + lane + 32 * j] : 0.0;
-  double* out = L.is_leaf ? nullptr : x_out + f * out_rows * ldr + col0;
+  double* out = (L.is_leaf || L.children_idle(f)) ? nullptr : x_out + f * out_rows * ldr + col0;
   if (mp) {
     for (int r0 = k; r0 < m; r0 += 4) {
       double v[4][CPL];
@@ -1762,6 +1762,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
     X[lane] = z;
   }
   __syncwarp();
+  if (L.children_idle(f)) return;  // children without pivots never read the block
   double* Xo = x_out + f * out_rows * ldr + col0;
   for (int rr = lane; rr < m; rr += 32) Xo[(long long)rr * ldr] = X[rr];
 }

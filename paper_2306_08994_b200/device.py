@@ -193,6 +193,7 @@ class DevicePlan:
             # pivot-free subtrees: the front has no pivots and neither has any
             # descendant, so its forward update block is zero (the solve skips it)
             z = lt.front_k() == 0
+            kids = None
             if zprev is not None:
                 kids = np.ones(lt.n_fronts, dtype=bool)
                 nc = len(zprev)
@@ -201,7 +202,12 @@ class DevicePlan:
                 has2 = 2 * i + 1 < nc
                 kids[has2] &= zprev[2 * i[has2] + 1]
                 z &= kids
-            dl.zero_upd = torch.from_numpy(z.astype(np.uint8)).to(self.device)
+            # bit 0: pivot-free subtree; bit 1: every child's subtree is pivot-free
+            # (no child reads the front's backward block: it is not written)
+            code = z.astype(np.uint8)
+            if kids is not None:
+                code |= kids.astype(np.uint8) << 1
+            dl.zero_upd = torch.from_numpy(code).to(self.device)
             dl.view.zero_upd = dl.zero_upd.data_ptr()
             # implicit forward updates: pivots but no child contribution
             dl.implicit = (lt.front_k() > 0) & (np.ones(lt.n_fronts, dtype=bool) if zprev is None
