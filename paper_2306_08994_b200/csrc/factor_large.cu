@@ -948,6 +948,15 @@ static cudaError_t launch_dataflow(const LevelArgs& L, double* factors, double t
                                    unsigned long long* err, int* ws_flags, int cb0, int TC,
                                    int TR, bool coop, cudaStream_t st);
 
+// Only the redundant-per-CTA diagonal-block kernels (large_block_kernel,
+// single-front levels; the dataflow chains) leave the panel's diagonal
+// blocks as assembled: the separate diagonal kernels (diag32 / diag64) write
+// l and d into the panel themselves, so the finalize copy is skipped for them.
+static bool need_finalize(long long level_fronts) {
+  return level_fronts <= kFusedBlockMaxFronts || chain_dataflow();
+}
+static bool diag_blocks_need_finalize(const LevelArgs& L) { return need_finalize(L.level_fronts); }
+
 static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd, double* factors,
                                     double* upd_out, double thr, unsigned long long* err,
                                     int* ws_flags, cudaStream_t st) {
@@ -1000,10 +1009,12 @@ static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd,
   cudaStreamWaitEvent(st, S.chain_done, 0);
   cudaStreamWaitEvent(st, S.panel_done, 0);
   cudaStreamWaitEvent(st, S.schur_done, 0);
-  dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
-  timer_begin(K_FINALIZE, st);
-  large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
-  timer_end(st);
+  if (diag_blocks_need_finalize(L)) {
+    dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
+    timer_begin(K_FINALIZE, st);
+    large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
+    timer_end(st);
+  }
   return cudaGetLastError();
 }
 
@@ -1594,7 +1605,7 @@ cudaError_t launch_factor_large(const LevelArgs& L, const double* child_upd, dou
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  if (L.max_k > 0) {
+  if (L.max_k > 0 && diag_blocks_need_finalize(L)) {
     dim3 g((unsigned)L.n_fronts, (unsigned)((L.max_k + NB - 1) / NB));
     timer_begin(K_FINALIZE, st);
     large_diag_finalize_kernel<<<g, 256, 0, st>>>(L, factors);
@@ -1623,7 +1634,7 @@ int large_level_launches(int max_k, int max_upd, long long level_fronts) {
   const int W = lookahead_width(max_upd);
   if (max_k > W && level_fronts <= kLookaheadMaxFronts) {
     const int nsb = (max_k + W - 1) / W;
-    int n = 2;  // assembly, finalize
+    int n = 1 + (need_finalize(level_fronts) ? 1 : 0);  // assembly, finalize
     for (int j = 0; j < nsb; j++) {
       const int c0 = j * W, c1 = std::min(c0 + W, max_k);
       n += large_panel_launches(c1 - c0, fronts) + (j + 1 < nsb) + (j + 2 < nsb) +
@@ -1632,7 +1643,7 @@ int large_level_launches(int max_k, int max_upd, long long level_fronts) {
     return n;
   }
   return 1 + large_panel_launches(max_k, fronts) + (max_k > 0 && max_upd > 0 ? 1 : 0) +
-         (max_k > 0 ? 1 : 0);
+         (max_k > 0 && need_finalize(level_fronts) ? 1 : 0);
 }
 
 cudaError_t set_jitter_factor(unsigned seed) { return set_jitter_tu(seed); }
