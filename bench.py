@@ -429,6 +429,11 @@ def run_ours(args, cfg):
                    "solve_ms": float(eager_ms - level_ms.sum()),
                    "launch": "one CUDA graph per step" if graph is not None else "eager",
                    "eager_ms_per_step": eager_ms,
+                   "top_slices": (None if world > 1 or dp._split_plan() is None else
+                                  {"levels": [dp._split_plan()[0], dp._split_plan()[1] - 1],
+                                   "slices": dp.split_top,
+                                   "note": "factored concurrently; level_ms of these levels "
+                                           "is reported on the first one"}),
                    "ldl_gflop": total_ldl / 1e9, "alg_bytes_gb": total_bytes / 1e9,
                    "l2": "working set >> 126 MB L2 (no flush needed)", "rel_residual": rel_res,
                    "parallelism": (f"subtree-sharded over {world} GPUs (NCCL P2P of root-ward "

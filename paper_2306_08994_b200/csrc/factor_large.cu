@@ -910,11 +910,16 @@ struct LookaheadStreams {
   cudaStream_t chain = nullptr, panel = nullptr, schur = nullptr;
   cudaEvent_t start, chain_done, panel_done, schur_done;
 };
-static LookaheadStreams& lookahead_streams() {  // one set per device
-  static LookaheadStreams all[64];
+// One set per device and per slice slot: slices of a level (front ranges,
+// front_base > 0) factored concurrently on different streams get their own
+// streams and events (slot = which eighth of the level the slice starts in).
+static LookaheadStreams& lookahead_streams(const LevelArgs& L) {
+  static LookaheadStreams all[64][8];
   int dev = 0;
   cudaGetDevice(&dev);
-  LookaheadStreams& ls = all[dev & 63];
+  const long long lf = std::max<long long>(L.level_fronts, 1);
+  const int slot = (int)std::min<long long>(7, std::max<long long>(0, L.front_base * 8 / lf));
+  LookaheadStreams& ls = all[dev & 63][slot];
   if (!ls.chain) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -960,7 +965,7 @@ static bool diag_blocks_need_finalize(const LevelArgs& L) { return need_finalize
 static cudaError_t factor_lookahead(const LevelArgs& L, const double* child_upd, double* factors,
                                     double* upd_out, double thr, unsigned long long* err,
                                     int* ws_flags, cudaStream_t st) {
-  LookaheadStreams& S = lookahead_streams();
+  LookaheadStreams& S = lookahead_streams(L);
   cudaEventRecord(S.start, st);  // after the assembly
   cudaStreamWaitEvent(S.chain, S.start, 0);
   cudaStreamWaitEvent(S.panel, S.start, 0);

@@ -228,6 +228,9 @@ class DevicePlan:
         self._fgraph = None   # (threshold, CUDA graph) of factor() (public API path)
         self._sgraphs = {}    # rhs shape -> (graph, static b, static x) of solve_into()
         self.fuse_bottom = True  # run the lowest levels as one subtree kernel when possible
+        self.split_top = int(os.environ.get("TFB_SPLIT_TOP", "2"))  # concurrent top slices
+        self.split_fronts = int(os.environ.get("TFB_SPLIT_FRONTS", "1024"))
+        self._split = None
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
     def _setup_implicit(self) -> None:
@@ -348,10 +351,92 @@ class DevicePlan:
             if level_hook is not None:
                 for L in range(nf):
                     level_hook(L)
-        for L in range(max(nf, 0) if nf >= 2 else 0, len(self.levels)):
+        sp_ = self._split_plan()
+        lo = max(nf, 0) if nf >= 2 else 0
+        S, R = sp_ if sp_ is not None else (len(self.levels), len(self.levels))
+        for L in range(lo, min(S, len(self.levels))):
             self.factor_level(L, threshold, sp)
             if level_hook is not None:
                 level_hook(L)
+        if sp_ is not None:
+            self._factor_split(threshold, st, S, R)
+            if level_hook is not None:
+                for L in range(S, R):
+                    level_hook(L)
+            for L in range(R, len(self.levels)):
+                self.factor_level(L, threshold, sp)
+                if level_hook is not None:
+                    level_hook(L)
+
+    # ---- concurrent top subtrees -------------------------------------------------
+    def _split_plan(self):
+        """(S, R): levels S .. R-1 are factored as `split_top` concurrent
+        slices (independent subtrees of the top levels, each on its own
+        stream with its own lookahead streams), the levels from R (fewer
+        fronts than slices) after them; None when off (TFB_SPLIT_TOP=1) or
+        the tree does not split evenly.  S is the lowest large level with at
+        most `split_fronts` fronts from which every level splits evenly (the
+        lookahead levels, whose pivot chains leave SMs idle)."""
+        H = self.split_top
+        n = len(self.levels)
+        if H < 2 or n < 3 or self.levels[-1].n_fronts != 1:
+            return None
+        # R: first level with fewer than H fronts (it and the levels above run whole)
+        R = next(L for L in range(n) if self.levels[L].n_fronts < H)
+
+        def even(S):
+            for L in range(S, R):
+                nl = self.levels[L].n_fronts
+                if nl % H or (L > S and self.levels[L - 1].n_fronts != 2 * nl):
+                    return False
+            return True
+        for S in range(1, R):  # the lowest qualifying level from which the top splits evenly
+            if self.levels[S].large and self.levels[S].n_fronts <= self.split_fronts and even(S):
+                return S, R
+        return None
+
+    def _factor_split(self, threshold: float, st, S: int, R: int) -> None:
+        from .distributed import _slice_view
+        H = self.split_top
+        if self._split is None or self._split[0] != (S, R, H):
+            streams = [torch.cuda.Stream(self.device) for _ in range(H)]
+            per = max([self.levels[L].n_fronts // H * self.levels[L].upd_stride
+                       for L in range(S, R - 1)] or [1])
+            bufs = [[_buf(per, self.device) for _ in range(2)] for _ in range(H)]
+            ws = [[(_buf(self.levels[L].ws_bytes, self.device, torch.uint8)
+                    if self.levels[L].ws_bytes > 0 else None) for L in range(n_)]
+                  for n_ in [len(self.levels)] * H]
+            self._split = ((S, R, H), streams, bufs, ws)
+        _, streams, bufs, ws = self._split
+        if GUARD:
+            poison(*[b for hb in bufs for b in hb])
+        for h in range(H):
+            streams[h].wait_stream(st)
+        for L in range(S, R):
+            dl = self.levels[L]
+            nl = dl.n_fronts // H
+            for h in range(H):
+                f0 = h * nl
+                cb = 0 if L == S else h * self.levels[L - 1].n_fronts // H
+                v = _slice_view(dl.view, f0, nl, child_base=cb)
+                fac = self.factors[L].data_ptr() + 8 * f0 * dl.fac_stride
+                v.factors = fac
+                if dl.aux is not None:
+                    v.aux = dl.aux.data_ptr() + 8 * f0 * dl.aux_stride
+                child = self.upd[(L - 1) & 1] if L == S else bufs[h][(L - 1) & 1]
+                if L == R - 1:  # the first whole level reads every child from one buffer
+                    out = self.upd[L & 1].data_ptr() + 8 * f0 * dl.upd_stride
+                else:
+                    out = bufs[h][L & 1].data_ptr()
+                w = ws[h][L]
+                rc = self.lib.tf_level_factor(C.byref(v), _ptr(child), _ptr(self.elem),
+                                              C.c_void_p(fac), C.c_void_p(out),
+                                              C.c_double(threshold), _ptr(self.err), _ptr(w),
+                                              dl.ws_bytes if w is not None else 0,
+                                              C.c_void_p(streams[h].cuda_stream))
+                _lib.check(rc, f"tf_level_factor(level {L}, slice {h})")
+        for h in range(H):
+            st.wait_stream(streams[h])
 
     def zero_pivot_position(self) -> int:
         """-1, or the pivot-order position of the earliest pivot at/below threshold."""
@@ -560,9 +645,14 @@ class DevicePlan:
         x.copy_(gx)
 
     def launches_per_factor(self) -> int:
-        """Kernel launches one factorization issues (tf_level_launch_count)."""
-        return sum(int(self.lib.tf_level_launch_count(C.byref(dl.view), 1, 0))
-                   for dl in self.levels)
+        """Kernel launches one factorization issues (tf_level_launch_count;
+        levels factored as concurrent slices launch their sequence per slice)."""
+        sp_ = self._split_plan()
+        n = 0
+        for L, dl in enumerate(self.levels):
+            c = int(self.lib.tf_level_launch_count(C.byref(dl.view), 1, 0))
+            n += c * (self.split_top if sp_ is not None and sp_[0] <= L < sp_[1] else 1)
+        return n
 
     def launches_per_solve(self, nrhs: int) -> int:
         n = 2  # permutations
