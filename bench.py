@@ -272,7 +272,9 @@ def run_ours(args, cfg):
     graph = None
     if sharded is None and not args.no_graph:
         # the whole factor + solve as one CUDA graph (DevicePlan.capture)
-        graph = dp.capture(thr, b, x, warmup=False)
+        # forward sweeps of the lower levels overlapped with the top levels'
+        # latency-bound factorization (DevicePlan.factor_solve)
+        graph = dp.capture(thr, b, x, warmup=False, overlap=not args.no_overlap)
         for _ in range(2):
             graph.replay()
         torch.cuda.synchronize()
@@ -428,6 +430,9 @@ def run_ours(args, cfg):
                    "levels": nl, "factor_ms": float(level_ms.sum()),
                    "solve_ms": float(eager_ms - level_ms.sum()),
                    "launch": "one CUDA graph per step" if graph is not None else "eager",
+                   "schedule": ("factor, then solve" if args.no_overlap else
+                                f"forward sweeps of the levels below the top "
+                                f"{dp.fwd_overlap_top} overlapped with their factorization"),
                    "eager_ms_per_step": eager_ms,
                    "top_slices": (None if world > 1 or dp._split_plan() is None else
                                   {"levels": [dp._split_plan()[0], dp._split_plan()[1] - 1],
@@ -464,6 +469,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="factor, then solve (no forward sweeps during the top levels)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel from the host each step instead of a CUDA graph")
     ap.add_argument("--small-max-m", type=int, default=None,

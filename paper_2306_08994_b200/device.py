@@ -231,6 +231,7 @@ class DevicePlan:
         self.split_top = int(os.environ.get("TFB_SPLIT_TOP", "2"))  # concurrent top slices
         self.split_fronts = int(os.environ.get("TFB_SPLIT_FRONTS", "1024"))
         self._split = None
+        self.fwd_overlap_top = int(os.environ.get("TFB_FWD_OVERLAP_TOP", "1"))
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
     def _setup_implicit(self) -> None:
@@ -508,13 +509,14 @@ class DevicePlan:
                      stream: Optional[torch.cuda.Stream] = None) -> None:
         """factor(threshold) then x = A^-1 b, with the forward sweep overlapped.
 
-        The forward sweep of level L needs only the factors of levels <= L, so
-        it runs on a second stream right after level L is factored, while the
-        factorization of the levels above proceeds (compute-bound Schur GEMMs
-        next to memory-bound sweeps).  Sweeps that use the cooperative
-        wavefront kernels (tf_level_solve_cooperative) wait for the whole
-        factorization, as does the backward sweep.  Same kernels and order
-        per stream as factor() + solve_into(): identical results."""
+        The forward sweep of level L needs only the factors of levels <= L.
+        The top levels' factorization is a latency-bound pivot chain (the
+        root's dataflow kernel leaves most SM issue slots idle), so the
+        forward sweeps of every level below the top `fwd_overlap_top` levels
+        run on a second stream while those top levels are factored
+        (TFB_FWD_OVERLAP_TOP, default 1: the root); the top levels' sweeps
+        and the backward sweep follow the factorization.  Same kernels and
+        order per stream as factor() + solve_into(): identical results."""
         st = stream or torch.cuda.current_stream(self.device)
         if self._side is None:
             self._side = torch.cuda.Stream(self.device)
@@ -526,22 +528,22 @@ class DevicePlan:
         ss.wait_stream(st)                       # b (and everything before) ready
         with torch.cuda.stream(ss):
             self._solve_begin(b, x, ssp)
-        state = {"next": 0, "open": True}
+        nl = len(self.levels)
+        top = min(max(self.fwd_overlap_top, 0), nl)
+        last = nl - 1 - top  # sweeps of levels <= last overlap the top levels' factorization
+        state = {"next": 0}
 
         def hook(L):
-            self._lvl_ev[L].record(st)
-            while state["open"] and state["next"] <= L:
-                n = state["next"]
-                if self.lib.tf_level_solve_cooperative(C.byref(self.levels[n].view), nrhs, 1):
-                    state["open"] = False
-                    break
-                ss.wait_event(self._lvl_ev[n])
-                self._solve_fwd_level(n, nrhs, ssp)
-                state["next"] = n + 1
+            if L == last:
+                self._lvl_ev[L].record(st)
+                ss.wait_event(self._lvl_ev[L])
+                for n in range(last + 1):
+                    self._solve_fwd_level(n, nrhs, ssp)
+                state["next"] = last + 1
 
-        self.factor(threshold, st, level_hook=hook)
+        self.factor(threshold, st, level_hook=hook if last >= 0 else None)
         ss.wait_stream(st)
-        for L in range(state["next"], len(self.levels)):
+        for L in range(state["next"], nl):
             self._solve_fwd_level(L, nrhs, ssp)
         self._solve_end(x, nrhs, ssp)
         st.wait_stream(ss)
