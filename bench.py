@@ -412,6 +412,8 @@ def run_ours(args, cfg):
     roof["kernel"] = name
     roof["launches_per_step"] = k_n / args.steps
     roof["share_of_kernel_time"] = k_ms / max(tot_ms, 1e-9)
+    roof["time_basis"] = ("CUDA events around every launch of the class on its stream, "
+                          "union of the launch intervals (concurrent launches counted once)")
     roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
                            "measured cuBLAS DGEMM 35.47 TF/s (profiles/r01_dgemm_cublas_peak.log)")
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in

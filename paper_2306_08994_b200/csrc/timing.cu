@@ -1,7 +1,9 @@
 // Optional per-kernel-class device timing (CUDA events on the launch stream),
 // used by bench.py to report the dominant kernel's roofline from the timed
 // region itself.  Off by default: then begin/end are a single branch.
+#include <algorithm>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -56,17 +58,42 @@ using namespace tfb;
 
 extern "C" void tf_timing_enable(int32_t on) { g_on = on != 0; }
 
+// Per class: the device time during which at least one of its launches was
+// in flight (union of the launches' [begin, end] intervals, so launches of
+// one class running concurrently on different streams -- lookahead chunks,
+// concurrent top slices -- are not counted twice), and the launch count.
 extern "C" int32_t tf_timing_collect(double* ms, int64_t* count, int32_t n) {
   if (ms) std::memset(ms, 0, sizeof(double) * n);
   if (count) std::memset(count, 0, sizeof(int64_t) * n);
-  for (const Pending& p : g_pending) {
-    cudaEventSynchronize(p.b);
-    float t = 0.f;
-    cudaEventElapsedTime(&t, p.a, p.b);
-    if (p.cls < n) {
-      if (ms) ms[p.cls] += t;
-      if (count) count[p.cls] += 1;
+  std::vector<std::vector<std::pair<float, float>>> iv(K_COUNT);
+  if (!g_pending.empty()) {
+    const cudaEvent_t ref = g_pending.front().a;
+    for (const Pending& p : g_pending) {
+      cudaEventSynchronize(p.b);
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, ref, p.a);
+      cudaEventElapsedTime(&t1, ref, p.b);
+      if (p.cls >= 0 && p.cls < K_COUNT) iv[p.cls].push_back({t0, t1});
     }
+  }
+  for (int c = 0; c < K_COUNT && c < n; c++) {
+    auto& v = iv[c];
+    std::sort(v.begin(), v.end());
+    double tot = 0.0, s = 0.0, e = -1.0;
+    for (const auto& x : v) {
+      if (x.first > e) {
+        if (e > s) tot += e - s;
+        s = x.first;
+        e = x.second;
+      } else if (x.second > e) {
+        e = x.second;
+      }
+    }
+    if (e > s) tot += e - s;
+    if (ms) ms[c] = tot;
+    if (count) count[c] = (int64_t)v.size();
+  }
+  for (const Pending& p : g_pending) {
     g_pool.push_back(p.a);
     g_pool.push_back(p.b);
   }

@@ -232,6 +232,7 @@ class DevicePlan:
         self.split_fronts = int(os.environ.get("TFB_SPLIT_FRONTS", "1024"))
         self._split = None
         self.fwd_overlap_top = int(os.environ.get("TFB_FWD_OVERLAP_TOP", "1"))
+        self.implicit_min_nrhs = int(os.environ.get("TFB_IMPLICIT_MIN_NRHS", "1"))
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
 
     def _setup_implicit(self) -> None:
@@ -458,6 +459,13 @@ class DevicePlan:
 
     def _solve_begin(self, b: torch.Tensor, x: torch.Tensor, sp) -> int:
         nrhs = 1 if b.dim() == 1 else b.shape[1]
+        # implicit forward updates pay off only with several columns (the
+        # parent re-reads the child's panel rows, k per update row, instead of
+        # one update row per column): on below implicit_min_nrhs columns
+        on = nrhs >= self.implicit_min_nrhs
+        for dl in self.levels:
+            t = getattr(dl, "implicit_t", None)
+            dl.view.implicit_upd = t.data_ptr() if (on and t is not None) else None
         blk = self._blocks(nrhs)
         if GUARD:
             poison(*blk, self._y)  # (the workspace's flags must start at zero: not poisoned)
