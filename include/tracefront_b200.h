@@ -266,6 +266,23 @@ int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* parent,
                        double* x_out, int64_t out_rows, double* y, int32_t nrhs,
                        void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Tiny trees (1D meshes, small 2D ones): the whole factorization (every
+ * level of tf_level_factor) and, optionally, a single-RHS solve (permute,
+ * every forward and backward level sweep, scatter back) in ONE launch of one
+ * CTA -- the per-level launches, not the work, are the cost there.  views:
+ * all levels (factors attached, whole levels); upd0/upd1: the ping-pong
+ * update buffers (level L writes upd[L & 1]); perm/n_pivots: the pivot order
+ * (1-based, tf_plan_pivot_order); b -> x (n_dof, may alias); y: n_pivots
+ * scratch; blk0/blk1: solve blocks (n_fronts * max_m doubles per level).
+ * tf_tree_small_ok: 1 when the tree qualifies (levels all shared-memory
+ * levels with small fronts, <= 4096 leaves). */
+int32_t tf_tree_small_ok(const tf_level_view* views, int32_t n_levels);
+int tf_tree_factor_solve(const tf_level_view* views, int32_t n_levels, const double* elem,
+                         double* upd0, double* upd1, double threshold, unsigned long long* err,
+                         const int32_t* perm, int64_t n_pivots, int64_t n_dof, const double* b,
+                         double* x, double* y, double* blk0, double* blk1, int32_t do_factor,
+                         int32_t do_solve, void* stream);
+
 /* Workspace bytes tf_level_solve_fwd / tf_level_solve_bwd need for this level and nrhs. */
 int64_t tf_level_solve_workspace(const tf_level_view* lv, int32_t nrhs);
 

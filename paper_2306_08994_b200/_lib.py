@@ -79,6 +79,7 @@ EXPORTS = (
     "tf_subtree_factor", "tf_timing_enable", "tf_timing_collect", "tf_timing_class_name",
     "tf_build_info", "tf_atomic_fnf", "tf_mesh_tensor_device_workspace",
     "tf_mesh_tensor_device", "tf_mesh_element_values_device", "tf_level_solve_cooperative",
+    "tf_tree_small_ok", "tf_tree_factor_solve",
 )
 
 _lib = None
@@ -142,6 +143,11 @@ def load() -> C.CDLL:
     lib.tf_mesh_element_values_device.restype = C.c_int
     lib.tf_level_solve_cooperative.argtypes = [C.POINTER(LevelView), i32, i32]
     lib.tf_level_solve_cooperative.restype = i32
+    lib.tf_tree_small_ok.argtypes = [vp, i32]
+    lib.tf_tree_small_ok.restype = i32
+    lib.tf_tree_factor_solve.argtypes = [vp, i32, vp, vp, vp, C.c_double, vp, vp, i64, i64, vp,
+                                         vp, vp, vp, vp, i32, i32, vp]
+    lib.tf_tree_factor_solve.restype = C.c_int
     lib.tf_set_jitter.argtypes = [C.c_uint32]
     lib.tf_set_jitter.restype = C.c_int
     lib.tf_set_small_max_m.argtypes = [i32]

@@ -27,6 +27,13 @@ int subtree_fusable_levels(const LevelArgs* lv, int n_levels);
 cudaError_t launch_factor_subtree(const LevelArgs* lv, int nlev, double* const* fac,
                                   const double* elem, double* upd_out, double thr,
                                   unsigned long long* err, cudaStream_t st);
+struct TreeArgs;
+size_t tree_small_smem(const LevelArgs* lv, int nlev, TreeArgs* A);
+cudaError_t launch_tree_small(const LevelArgs* lv, int nlev, const double* elem, double* upd0,
+                              double* upd1, double thr, unsigned long long* err, const int* perm,
+                              long long n_piv, long long n_dof, const double* b, double* x,
+                              double* y, double* blk0, double* blk1, int do_factor, int do_solve,
+                              cudaStream_t st);
 int large_level_launches(int max_k, int max_upd, long long level_fronts);
 int solve_launches(const LevelArgs& L, int nrhs, bool fwd);
 int solve_cooperative(const LevelArgs& L, int nrhs, bool fwd);
@@ -138,6 +145,30 @@ extern "C" int tf_level_solve_bwd(const tf_level_view* lv, const tf_level_view* 
   return status(launch_solve_bwd(L, PA, parent ? 1 : 0, factors, x_parent, parent_rows, x_out,
                                  out_rows, y, nrhs, (double*)workspace, workspace_bytes / 8,
                                  (cudaStream_t)stream));
+}
+
+extern "C" int32_t tf_tree_small_ok(const tf_level_view* views, int32_t n_levels) {
+  if (!views || n_levels < 1 || n_levels > 24) return 0;
+  LevelArgs lv[24];
+  for (int L = 0; L < n_levels; L++) lv[L] = make_args(&views[L]);
+  return tree_small_smem(lv, n_levels, nullptr) > 0 ? 1 : 0;
+}
+
+extern "C" int tf_tree_factor_solve(const tf_level_view* views, int32_t n_levels,
+                                    const double* elem, double* upd0, double* upd1,
+                                    double threshold, unsigned long long* err, const int32_t* perm,
+                                    int64_t n_pivots, int64_t n_dof, const double* b, double* x,
+                                    double* y, double* blk0, double* blk1, int32_t do_factor,
+                                    int32_t do_solve, void* stream) {
+  if (!views || n_levels < 1 || n_levels > 24) return TF_ERR_INVALID;
+  if (do_factor && (!elem || !upd0 || !upd1 || !err)) return TF_ERR_INVALID;
+  if (do_solve && (!perm || !b || !x || !y || !blk0 || !blk1)) return TF_ERR_INVALID;
+  LevelArgs lv[24];
+  for (int L = 0; L < n_levels; L++) lv[L] = make_args(&views[L]);
+  if (tree_small_smem(lv, n_levels, nullptr) == 0) return TF_ERR_INVALID;
+  return status(launch_tree_small(lv, n_levels, elem, upd0, upd1, threshold, err, perm, n_pivots,
+                                  n_dof, b, x, y, blk0, blk1, do_factor, do_solve,
+                                  (cudaStream_t)stream));
 }
 
 extern "C" int tf_permute_rows(const int32_t* idx, int64_t n, const double* in, double* out,

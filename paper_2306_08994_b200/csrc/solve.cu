@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "front_small.cuh"
 
 namespace tfb {
 
@@ -2250,6 +2251,134 @@ int solve_launches(const LevelArgs& L, int nrhs, bool fwd) {
   const int slices = (nrhs + kWaveCols - 1) / kWaveCols;
   if (fwd) return slices;
   return 1 + (L.max_k > 0 ? slices : 0);
+}
+
+// ------------------------------------------------------------- tiny trees
+// The whole factorization and single-RHS solve of a small tree whose levels
+// are all shared-memory levels (1D meshes, small 2D ones) in ONE launch of one
+// CTA: there the ~3 launches per level, not the work, are the cost.  Per
+// level the CTA's threads stride over its fronts, one thread per front
+// (factor_front<1>, solve_*_small_front<1>: the level kernels' per-front code
+// with a group of one), a CTA barrier between levels; the permutations to and
+// from pivot order are in the same launch.
+constexpr int kTreeMaxLevels = 24;
+constexpr int kTreeThreads = 1024;  // at most; fewer when the fronts need more scratch
+constexpr int kTreeMaxLeaves = 4096;
+constexpr size_t kTreeSmemMax = 200 * 1024;
+struct TreeArgs {
+  LevelArgs lv[kTreeMaxLevels];
+  double* fac[kTreeMaxLevels];
+  int nlev;
+  int fsmem;    // doubles per thread: factor front scratch
+  int ssmem;    // doubles per thread: solve vector block
+  int threads;  // CTA size
+};
+
+__global__ void __launch_bounds__(kTreeThreads)
+    tree_small_kernel(TreeArgs A, const double* __restrict__ elem, double* upd0, double* upd1,
+                      double thr, unsigned long long* err, const int* __restrict__ perm,
+                      long long n_piv, long long n_dof, const double* b, double* x, double* y,
+                      double* blk0, double* blk1, int do_factor, int do_solve) {
+  extern __shared__ __align__(16) double tsm[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(tsm);
+  const int t = threadIdx.x, nt = blockDim.x;
+  if (do_solve) {
+    for (long long i = t; i < n_dof; i += nt) x[i] = b[i];  // DOFs outside every front
+    for (long long i = t; i < n_piv; i += nt) y[i] = b[perm[i] - 1];
+    __syncthreads();
+  }
+  // one phase per level: factor the level's fronts, then (same thread, same
+  // fronts: its factors are its own writes) their forward sweep
+  double* F = tsm + (size_t)t * A.fsmem;
+  const int per = A.ssmem * 8;
+  for (int L = 0; L < A.nlev; L++) {
+    const LevelArgs& lv = A.lv[L];
+    if (do_factor) {
+      const double* child = (L & 1) ? upd0 : upd1;  // level L-1 wrote upd[(L-1) & 1]
+      double* out = (L & 1) ? upd1 : upd0;
+      double* lvec = F + small_front_doubles(lv.max_m, lv.max_k) - lv.max_m;
+      for (long long f = t; f < lv.n_fronts; f += nt) {
+        const Shape S = front_shape(lv, f);
+        const double* s0 = lv.is_leaf ? elem + f * lv.elem_stride
+                                      : child + lv.child_slot(f, 0) * lv.child_upd_stride;
+        const double* s1 =
+            lv.is_leaf ? nullptr : child + lv.child_slot(f, 1) * lv.child_upd_stride;
+        factor_front<1>(lv, f, S, s0, s1, elem, F, lvec, A.fac[L] + f * lv.fac_stride,
+                        out + f * lv.upd_stride, thr, err, 0, 0, 1 << 30);
+      }
+    }
+    if (do_solve) {
+      const LevelArgs& C = A.lv[L > 0 ? L - 1 : 0];
+      const double* w_child = ((L - 1) & 1) ? blk1 : blk0;
+      double* w_out = (L & 1) ? blk1 : blk0;
+      for (long long f = t; f < lv.n_fronts; f += nt)
+        solve_fwd_small_front<1, kTreeThreads, false>(f, lv, C, A.fac[L], w_child, C.max_m, 1,
+                                                     w_out, lv.max_m, y, 1, 1, 0, per, sm);
+    }
+    __syncthreads();
+  }
+  if (!do_solve) return;
+  for (int L = A.nlev - 1; L >= 0; L--) {
+    const LevelArgs& lv = A.lv[L];
+    const bool hp = L + 1 < A.nlev;
+    const LevelArgs& PA = A.lv[hp ? L + 1 : L];
+    const double* x_parent = ((L + 1) & 1) ? blk1 : blk0;
+    double* x_out = (L & 1) ? blk1 : blk0;
+    for (long long f = t; f < lv.n_fronts; f += nt)
+      solve_bwd_small_front<1, kTreeThreads, false>(f, lv, PA, hp ? 1 : 0, A.fac[L], x_parent,
+                                                   PA.max_m, x_out, lv.max_m, y, 1, 1, 0, per,
+                                                   sm);
+    __syncthreads();
+  }
+  for (long long i = t; i < n_piv; i += nt) x[perm[i] - 1] = y[i];
+}
+
+// Shared memory of the tiny-tree kernel (0: the tree does not qualify).
+size_t tree_small_smem(const LevelArgs* lv, int nlev, TreeArgs* A) {
+  if (nlev < 1 || nlev > kTreeMaxLevels || lv[0].n_fronts > kTreeMaxLeaves) return 0;
+  int fs = 0, ss = 0;
+  for (int L = 0; L < nlev; L++) {
+    if (level_is_large(lv[L].is_leaf, lv[L].max_m) || lv[L].front_base != 0 || !lv[L].factors)
+      return 0;
+    fs = std::max(fs, (small_front_doubles(lv[L].max_m, lv[L].max_k) + 1) & ~1);
+    ss = std::max(ss, (lv[L].max_m + 1) & ~1);
+  }
+  // threads: one per leaf front when the scratch fits (levels have at most as
+  // many fronts as the leaves), at least 256
+  int nt = kTreeThreads;
+  while (nt > 256 && ((size_t)nt * 8 * std::max(fs, ss) > kTreeSmemMax || nt / 2 >= lv[0].n_fronts))
+    nt /= 2;
+  const size_t smem = (size_t)nt * 8 * std::max(fs, ss);
+  if (smem > kTreeSmemMax) return 0;
+  if (A) {
+    A->threads = nt;
+    A->nlev = nlev;
+    A->fsmem = fs;
+    A->ssmem = ss;
+    for (int L = 0; L < nlev; L++) {
+      A->lv[L] = lv[L];
+      A->fac[L] = const_cast<double*>(lv[L].factors);
+    }
+  }
+  return smem;
+}
+
+cudaError_t launch_tree_small(const LevelArgs* lv, int nlev, const double* elem, double* upd0,
+                              double* upd1, double thr, unsigned long long* err, const int* perm,
+                              long long n_piv, long long n_dof, const double* b, double* x,
+                              double* y, double* blk0, double* blk1, int do_factor, int do_solve,
+                              cudaStream_t st) {
+  TreeArgs A;
+  const size_t smem = tree_small_smem(lv, nlev, &A);
+  if (!smem) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(tree_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  timer_begin(K_SUBTREE, st);
+  tree_small_kernel<<<1, A.threads, smem, st>>>(A, elem, upd0, upd1, thr, err, perm, n_piv,
+                                                    n_dof, b, x, y, blk0, blk1, do_factor,
+                                                    do_solve);
+  timer_end(st);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_permute_rows(const int* idx, long long n, const double* in, double* out,

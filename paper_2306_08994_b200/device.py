@@ -231,6 +231,7 @@ class DevicePlan:
         self.split_top = int(os.environ.get("TFB_SPLIT_TOP", "2"))  # concurrent top slices
         self.split_fronts = int(os.environ.get("TFB_SPLIT_FRONTS", "1024"))
         self._split = None
+        self._tiny_ok = None  # whole tree in one launch (tf_tree_small_ok), decided once
         self.fwd_overlap_top = int(os.environ.get("TFB_FWD_OVERLAP_TOP", "1"))
         self.implicit_min_nrhs = int(os.environ.get("TFB_IMPLICIT_MIN_NRHS", "1"))
         self.fuse_cap = FUSE_CAP_DEFAULT  # max fused levels (TFB_FUSE_LEVELS overrides)
@@ -341,6 +342,12 @@ class DevicePlan:
         self.err.fill_(-1)
         if GUARD:
             poison(*self.factors, *self.upd, *[dl.aux for dl in self.levels])
+        if self._tiny():
+            self._tree_call(threshold, None, None, 1, 0, sp)
+            if level_hook is not None:
+                for L in range(len(self.levels)):
+                    level_hook(L)
+            return
         nf = self.fused_levels
         if nf >= 2:
             views = (_lib.LevelView * nf)(*[dl.view for dl in self.levels[:nf]])
@@ -369,6 +376,33 @@ class DevicePlan:
                 self.factor_level(L, threshold, sp)
                 if level_hook is not None:
                     level_hook(L)
+
+    # ---- tiny trees: one launch --------------------------------------------------
+    def _tiny(self) -> bool:
+        """The whole tree qualifies for the one-launch kernel
+        (tf_tree_small_ok; TFB_TINY_TREE=0 disables)."""
+        if self._tiny_ok is None:
+            self.factors  # the kernel reads the factor pointers from the views
+            arr = (_lib.LevelView * len(self.levels))(*[dl.view for dl in self.levels])
+            self._tiny_ok = (os.environ.get("TFB_TINY_TREE", "1") != "0" and
+                             bool(self.lib.tf_tree_small_ok(C.cast(arr, C.c_void_p),
+                                                            len(self.levels))))
+        return self._tiny_ok
+
+    def _tree_call(self, threshold: float, b, x, do_factor: int, do_solve: int, sp) -> None:
+        arr = (_lib.LevelView * len(self.levels))(*[dl.view for dl in self.levels])
+        if do_solve:
+            blk = self._blocks(1)
+            if GUARD:
+                poison(*blk, self._y)
+        rc = self.lib.tf_tree_factor_solve(
+            C.cast(arr, C.c_void_p), len(self.levels), _ptr(self.elem), _ptr(self.upd[0]),
+            _ptr(self.upd[1]), C.c_double(threshold), _ptr(self.err),
+            _ptr(self.pivot_order) if do_solve else None, self.n_pivots, self.n_dof,
+            _ptr(b), _ptr(x), _ptr(self._y) if do_solve else None,
+            _ptr(self._blk[0]) if do_solve else None, _ptr(self._blk[1]) if do_solve else None,
+            do_factor, do_solve, sp)
+        _lib.check(rc, "tf_tree_factor_solve")
 
     # ---- concurrent top subtrees -------------------------------------------------
     def _split_plan(self):
@@ -508,6 +542,9 @@ class DevicePlan:
         """x = A^-1 b for row-major (n, nrhs) device tensors (b may alias x)."""
         st = stream or torch.cuda.current_stream(self.device)
         sp = C.c_void_p(st.cuda_stream)
+        if (b.dim() == 1 or b.shape[1] == 1) and self._tiny():
+            self._tree_call(0.0, b, x, 0, 1, sp)
+            return
         nrhs = self._solve_begin(b, x, sp)
         for L in range(len(self.levels)):
             self._solve_fwd_level(L, nrhs, sp)
@@ -526,6 +563,12 @@ class DevicePlan:
         and the backward sweep follow the factorization.  Same kernels and
         order per stream as factor() + solve_into(): identical results."""
         st = stream or torch.cuda.current_stream(self.device)
+        if (b.dim() == 1 or b.shape[1] == 1) and self._tiny():
+            self.err.fill_(-1)
+            if GUARD:
+                poison(*self.factors, *self.upd)
+            self._tree_call(threshold, b, x, 1, 1, C.c_void_p(st.cuda_stream))
+            return
         if self._side is None:
             self._side = torch.cuda.Stream(self.device)
             self._lvl_ev = [torch.cuda.Event() for _ in self.levels]
@@ -657,6 +700,8 @@ class DevicePlan:
     def launches_per_factor(self) -> int:
         """Kernel launches one factorization issues (tf_level_launch_count;
         levels factored as concurrent slices launch their sequence per slice)."""
+        if self._tiny():
+            return 1
         sp_ = self._split_plan()
         n = 0
         for L, dl in enumerate(self.levels):
@@ -665,6 +710,8 @@ class DevicePlan:
         return n
 
     def launches_per_solve(self, nrhs: int) -> int:
+        if nrhs == 1 and self._tiny():
+            return 1
         n = 2  # permutations
         for dl in self.levels:
             n += int(self.lib.tf_level_launch_count(C.byref(dl.view), nrhs, 1))
