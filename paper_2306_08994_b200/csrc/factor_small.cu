@@ -32,6 +32,18 @@ int small_smem_per_group(int max_m, int max_k) {
   return (int)((sizeof(double) * (size_t)small_front_doubles(max_m, max_k) + 15) & ~(size_t)15);
 }
 
+// Per-group stride of the level kernel (bytes): a group of G < 16 threads
+// touches G consecutive doubles at a time, so the groups of a warp are
+// staggered by G double-banks (stride = G mod 16 doubles) and together cover
+// all 16 banks -- with a stride that is a multiple of 16 doubles they would
+// pile onto the same G banks (measured: 50% excess shared wavefronts).
+static int small_group_stride(int max_m, int max_k, int G) {
+  int d = (small_smem_per_group(max_m, max_k) + 7) / 8;  // doubles, even
+  if (G < 16)
+    while ((d & 15) != (G & 15)) d += 2;
+  return d * 8;
+}
+
 template <int G, int GPC>
 __global__ void __launch_bounds__(G* GPC)
     factor_small_kernel(LevelArgs L, const double* __restrict__ child_upd,
@@ -61,7 +73,7 @@ template <int G, int GPC>
 static cudaError_t launch_small_t(const LevelArgs& L, const double* child_upd, const double* elem,
                                   double* factors, double* upd_out, double thr,
                                   unsigned long long* err, cudaStream_t st) {
-  const int per = small_smem_per_group(L.max_m, L.max_k);
+  const int per = small_group_stride(L.max_m, L.max_k, G);
   const size_t smem = (size_t)per * GPC;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = factor_small_kernel<G, GPC>;

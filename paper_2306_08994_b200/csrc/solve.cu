@@ -1909,7 +1909,15 @@ static cudaError_t launch_small_solve(const LevelArgs& L, const LevelArgs& O, in
                                       long long in_rows, double* w_out, long long out_rows,
                                       double* y, int nr, int ldr, int col0, cudaStream_t st) {
   const size_t pan = STAGE ? (size_t)L.max_m * L.max_k + L.max_m : 0;
-  const int per = (int)(((size_t)L.max_m * nr + pan) * 8 + 15) & ~15;
+  // per-group stride in doubles = G mod 16 (G < 16): the groups of a warp
+  // are staggered over the shared-memory banks (an odd stride for G = 1)
+  int per_d = (int)((size_t)L.max_m * nr + pan);
+  if (G < 16) {
+    while ((per_d & 15) != (G & 15)) per_d++;
+  } else {
+    per_d = (per_d + 1) & ~1;
+  }
+  const int per = per_d * 8;
   const size_t smem = (size_t)per * GPC;
   const unsigned full = (unsigned)((L.n_fronts + GPC - 1) / GPC);
   // leaf levels: nearly every front is pivot-free (returns at once): a few
