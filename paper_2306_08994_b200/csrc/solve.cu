@@ -2288,7 +2288,6 @@ __global__ void __launch_bounds__(kTreeThreads)
                       long long n_piv, long long n_dof, const double* b, double* x, double* y,
                       double* blk0, double* blk1, int do_factor, int do_solve) {
   extern __shared__ __align__(16) double tsm[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(tsm);
   const int t = threadIdx.x, nt = blockDim.x;
   if (do_solve) {
     for (long long i = t; i < n_dof; i += nt) x[i] = b[i];  // DOFs outside every front
@@ -2297,7 +2296,10 @@ __global__ void __launch_bounds__(kTreeThreads)
   }
   // one phase per level: factor the level's fronts, then (same thread, same
   // fronts: its factors are its own writes) their forward sweep
+  // separate scratch regions: a thread may run a front's forward sweep while
+  // another still factors in the same phase
   double* F = tsm + (size_t)t * A.fsmem;
+  unsigned char* ssm = reinterpret_cast<unsigned char*>(tsm + (size_t)nt * A.fsmem);
   const int per = A.ssmem * 8;
   for (int L = 0; L < A.nlev; L++) {
     const LevelArgs& lv = A.lv[L];
@@ -2321,7 +2323,7 @@ __global__ void __launch_bounds__(kTreeThreads)
       double* w_out = (L & 1) ? blk1 : blk0;
       for (long long f = t; f < lv.n_fronts; f += nt)
         solve_fwd_small_front<1, kTreeThreads, false>(f, lv, C, A.fac[L], w_child, C.max_m, 1,
-                                                     w_out, lv.max_m, y, 1, 1, 0, per, sm);
+                                                     w_out, lv.max_m, y, 1, 1, 0, per, ssm);
     }
     __syncthreads();
   }
@@ -2335,7 +2337,7 @@ __global__ void __launch_bounds__(kTreeThreads)
     for (long long f = t; f < lv.n_fronts; f += nt)
       solve_bwd_small_front<1, kTreeThreads, false>(f, lv, PA, hp ? 1 : 0, A.fac[L], x_parent,
                                                    PA.max_m, x_out, lv.max_m, y, 1, 1, 0, per,
-                                                   sm);
+                                                   ssm);
     __syncthreads();
   }
   for (long long i = t; i < n_piv; i += nt) x[perm[i] - 1] = y[i];
@@ -2354,9 +2356,9 @@ size_t tree_small_smem(const LevelArgs* lv, int nlev, TreeArgs* A) {
   // threads: one per leaf front when the scratch fits (levels have at most as
   // many fronts as the leaves), at least 256
   int nt = kTreeThreads;
-  while (nt > 256 && ((size_t)nt * 8 * std::max(fs, ss) > kTreeSmemMax || nt / 2 >= lv[0].n_fronts))
+  while (nt > 256 && ((size_t)nt * 8 * (fs + ss) > kTreeSmemMax || nt / 2 >= lv[0].n_fronts))
     nt /= 2;
-  const size_t smem = (size_t)nt * 8 * std::max(fs, ss);
+  const size_t smem = (size_t)nt * 8 * (fs + ss);
   if (smem > kTreeSmemMax) return 0;
   if (A) {
     A->threads = nt;
