@@ -308,9 +308,9 @@ class DevicePlan:
         return self._upd
 
     # ---- factorization -----------------------------------------------------------
-    def factor_level(self, L: int, threshold: float, sp) -> None:
+    def factor_level(self, L: int, threshold: float, sp, child=None) -> None:
         dl = self.levels[L]
-        prev = self.upd[(L - 1) & 1] if L > 0 else None
+        prev = child if child is not None else (self.upd[(L - 1) & 1] if L > 0 else None)
         rc = self.lib.tf_level_factor(C.byref(dl.view), _ptr(prev), _ptr(self.elem),
                                       _ptr(self.factors[L]), _ptr(self.upd[L & 1]),
                                       C.c_double(threshold), _ptr(self.err), _ptr(dl.ws),
@@ -373,7 +373,8 @@ class DevicePlan:
                 for L in range(S, R):
                     level_hook(L)
             for L in range(R, len(self.levels)):
-                self.factor_level(L, threshold, sp)
+                # level R reads the slices' last level from the boundary buffer
+                self.factor_level(L, threshold, sp, child=self._split[4] if L == R else None)
                 if level_hook is not None:
                     level_hook(L)
 
@@ -442,10 +443,14 @@ class DevicePlan:
             ws = [[(_buf(self.levels[L].ws_bytes, self.device, torch.uint8)
                     if self.levels[L].ws_bytes > 0 else None) for L in range(n_)]
                   for n_ in [len(self.levels)] * H]
-            self._split = ((S, R, H), streams, bufs, ws)
-        _, streams, bufs, ws = self._split
+            # the last sliced level writes a buffer of its own: the shared
+            # ping-pong buffer of its parity may still be read by the other
+            # slice's first level
+            bnd = _buf(self.levels[R - 1].n_fronts * self.levels[R - 1].upd_stride, self.device)
+            self._split = ((S, R, H), streams, bufs, ws, bnd)
+        _, streams, bufs, ws, bnd = self._split
         if GUARD:
-            poison(*[b for hb in bufs for b in hb])
+            poison(*[b for hb in bufs for b in hb], bnd)
         for h in range(H):
             streams[h].wait_stream(st)
         for L in range(S, R):
@@ -461,7 +466,7 @@ class DevicePlan:
                     v.aux = dl.aux.data_ptr() + 8 * f0 * dl.aux_stride
                 child = self.upd[(L - 1) & 1] if L == S else bufs[h][(L - 1) & 1]
                 if L == R - 1:  # the first whole level reads every child from one buffer
-                    out = self.upd[L & 1].data_ptr() + 8 * f0 * dl.upd_stride
+                    out = bnd.data_ptr() + 8 * f0 * dl.upd_stride
                 else:
                     out = bufs[h][L & 1].data_ptr()
                 w = ws[h][L]
