@@ -202,29 +202,49 @@ schur:
     group_sync<G>(bar);
     const double* P21 = F + tk;
     if constexpr (G >= 32) {
+      // a warp takes whole rows I of 8x8 tiles (rows I and T-1-I paired, so
+      // every pair has T+1 tiles): the row's A fragments (L21 D, k/4 DMMA
+      // steps) are loaded once and reused for its tiles J <= I
+      constexpr int KS = 4;  // k <= 16 in register fragments, longer k streamed
       const int warp = t >> 5, lane = t & 31, g8 = lane >> 2, tq = lane & 3;
-      const int T = (u + 7) >> 3, ntile = T * (T + 1) / 2;
-      for (int tile = warp; tile < ntile; tile += G / 32) {
-        int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-        I -= (I * (I + 1) / 2 > tile);
-        I += ((I + 1) * (I + 2) / 2 <= tile);
-        const int J = tile - I * (I + 1) / 2;
-        const int ia = 8 * I + g8, ib = 8 * J + g8;
+      const int T = (u + 7) >> 3, nw = G / 32;
+      auto tile_row = [&](int I) {
+        const int ia = 8 * I + g8;
         const double* arow = P21 + min(ia, u - 1) * ks;
-        const double* brow = P21 + min(ib, u - 1) * ks;
-        const bool va = ia < u, vb = ib < u;
-        double acc[2] = {0.0, 0.0};
-        for (int kk = 0; kk < k; kk += 4) {
-          const int q = kk + tq;
-          const double av = (va && q < k) ? arow[q] * lv[q] : 0.0;
-          const double bv = (vb && q < k) ? brow[q] : 0.0;
-          dmma884(acc, av, bv);
-        }
+        const bool va = ia < u;
+        double af[KS];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int jc = 8 * J + 2 * tq + h;
-          if (ia < u && jc <= ia) Sb[tri32(ia, jc)] -= acc[h];
+        for (int s4 = 0; s4 < KS; s4++) {
+          const int q = 4 * s4 + tq;
+          af[s4] = (va && q < k) ? arow[q] * lv[q] : 0.0;
         }
+        for (int J = 0; J <= I; J++) {
+          const int ib = 8 * J + g8;
+          const double* brow = P21 + min(ib, u - 1) * ks;
+          const bool vb = ib < u;
+          double acc[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s4 = 0; s4 < KS; s4++) {
+            if (4 * s4 < k) {
+              const int q = 4 * s4 + tq;
+              dmma884(acc, af[s4], (vb && q < k) ? brow[q] : 0.0);
+            }
+          }
+          for (int kk = 4 * KS; kk < k; kk += 4) {
+            const int q = kk + tq;
+            const double av = (va && q < k) ? arow[q] * lv[q] : 0.0;
+            dmma884(acc, av, (vb && q < k) ? brow[q] : 0.0);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int jc = 8 * J + 2 * tq + h;
+            if (ia < u && jc <= ia) Sb[tri32(ia, jc)] -= acc[h];
+          }
+        }
+      };
+      for (int pr = warp; pr < (T + 1) / 2; pr += nw) {
+        tile_row(pr);
+        if (T - 1 - pr != pr) tile_row(T - 1 - pr);
       }
     } else {
       int beg, end;
