@@ -251,13 +251,39 @@ schur:
       chunk_of(nS, G, t, beg, end);
       if (beg < end) {
         int a = tri_row32(beg), b = beg - (int)tri32(a, 0);
-        for (int e = beg; e < end; e++) {
-          const double* ra = P21 + a * ks;
-          const double* rb = P21 + b * ks;
-          double acc = 0.0;
-          for (int q = 0; q < k; q++) acc += ra[q] * lv[q] * rb[q];
-          Sb[e] -= acc;
-          if (++b > a) { a++; b = 0; }
+        if (k <= 4) {
+          // row a's scaled entries l(a,q) d_q stay in registers while the
+          // thread's contiguous chunk walks along the row (same products and
+          // summation order as below)
+          double wa[4];
+          auto load_row = [&](int r) {
+            const double* ra = P21 + r * ks;
+#pragma unroll
+            for (int q = 0; q < 4; q++) wa[q] = q < k ? ra[q] * lv[q] : 0.0;
+          };
+          load_row(a);
+          for (int e = beg; e < end; e++) {
+            const double* rb = P21 + b * ks;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              if (q < k) acc += wa[q] * rb[q];
+            Sb[e] -= acc;
+            if (++b > a) {
+              a++;
+              b = 0;
+              if (e + 1 < end) load_row(a);
+            }
+          }
+        } else {
+          for (int e = beg; e < end; e++) {
+            const double* ra = P21 + a * ks;
+            const double* rb = P21 + b * ks;
+            double acc = 0.0;
+            for (int q = 0; q < k; q++) acc += ra[q] * lv[q] * rb[q];
+            Sb[e] -= acc;
+            if (++b > a) { a++; b = 0; }
+          }
         }
       }
     }
