@@ -1168,13 +1168,25 @@ __global__ void permute_rows_kernel(const int* __restrict__ idx, long long n,
                                     const double* __restrict__ in, double* __restrict__ out,
                                     int nrhs, int scatter) {
   const long long total = n * nrhs;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long i = e / nrhs;
-    const int j = (int)(e - i * nrhs);
-    const long long g = (long long)idx[i] - 1;
-    if (scatter) out[g * nrhs + j] = in[e];
-    else out[e] = in[g * nrhs + j];
+  if (nrhs == 1) {  // one column: no row / column split (a 64-bit division per entry)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+      const long long g = (long long)__ldg(idx + i) - 1;
+      if (scatter) out[g] = in[i];
+      else out[i] = in[g];
+    }
+    return;
+  }
+  (void)total;
+  // several columns: a warp per row, lanes across the row's columns (coalesced)
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = w0; i < n; i += nw) {
+    const long long g = (long long)__ldg(idx + i) - 1;
+    const double* src = scatter ? in + i * nrhs : in + g * nrhs;
+    double* dst = scatter ? out + g * nrhs : out + i * nrhs;
+    for (int j = lane; j < nrhs; j += 32) dst[j] = src[j];
   }
 }
 
