@@ -113,6 +113,26 @@ def set_small_front_limit(m: int) -> int:
     return int(_lib.load().tf_set_small_max_m(int(m)))
 
 
+class _NoGC:
+    """Garbage collection off around a CUDA graph capture: a collector pass
+    during the capture can destroy an unreachable earlier graph (another
+    DevicePlan's), and destroying a graph while a stream captures invalidates
+    the capture ("operation not permitted when stream is capturing")."""
+
+    def __enter__(self):
+        import gc
+        self._was = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+        return False
+
+
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -626,7 +646,7 @@ class DevicePlan:
                     self.solve_into(b, x, stream)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
+        with _NoGC(), torch.cuda.graph(g, stream=stream):
             st = torch.cuda.current_stream(self.device)
             if overlap:  # forward sweep overlapped with the factorization (factor_solve)
                 self.factor_solve(threshold, b, x, st)
@@ -641,7 +661,7 @@ class DevicePlan:
         cs = torch.cuda.Stream(self.device)
         cs.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=cs):
+        with _NoGC(), torch.cuda.graph(g, stream=cs):
             fn(torch.cuda.current_stream(self.device))
         torch.cuda.current_stream(self.device).wait_stream(cs)
         return g

@@ -30,7 +30,7 @@ if (M / "cfg5_launches.csv").exists():
                          capture_output=True, text=True).stdout
     (P / "r02_cfg5_launches_summary.txt").write_text(
         "ncu launch list of `bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph` "
-        "(every launch of the run: warm-up, timed, diagnostic and end-to-end passes -- 9 "
+        "(every launch of the run: warm-up, timed, diagnostic, per-level and end-to-end "
         "factor+solve passes; ncu serializes the kernels; --clock-control none)\n" + out)
 if (M / "cfg5_traffic.csv").exists():
     out = subprocess.run([sys.executable, str(R / "tools" / "ncu_traffic.py"), str(M / "cfg5_traffic.csv"), "cfg5"],
