@@ -141,7 +141,8 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
         for (int r = c + 1 + t; r < k; r += G) {
           double* row = F + tri32(r, 0);
           const double lrc = row[c] * dinv;
-          for (int q = c + 1; q <= r; q++) row[q] -= lrc * F[tri32(q, c)];
+          int qc = tri32(c + 1, c);  // F[tri32(q, c)], stepped by q + 1
+          for (int q = c + 1; q <= r; qc += ++q) row[q] -= lrc * F[qc];
         }
         group_sync<G>(bar);
       }
@@ -179,7 +180,8 @@ __device__ __forceinline__ void factor_front(const LevelArgs& L, long long f, co
       double* row = F + rowp(r);
       const double lrc = row[c] * dinv;
       const int smax = min(r, k - 1);
-      for (int q = c + 1; q <= smax; q++) row[q] -= lrc * F[tri32(q, c)];
+      int qc = tri32(c + 1, c);  // F[tri32(q, c)], stepped by q + 1
+      for (int q = c + 1; q <= smax; qc += ++q) row[q] -= lrc * F[qc];
     }
     group_sync<G>(bar);
   }
