@@ -105,7 +105,7 @@ cudaError_t launch_factor_small(const LevelArgs& L, const double* child_upd, con
   // CTAs per SM (occupancy hides the shared-memory latency of the pivot loop)
   // (G, GPC) per front-order class m <= 4, 8, 16, 24, 48, 80, 232 (measured
   // on B200, tools/small_sweep.sh); TFB_SMALL_CFG="G:GPC,..." overrides
-  static int cfg[7][2] = {{2, 128}, {4, 64}, {8, 32}, {16, 16}, {32, 4}, {128, 1}, {256, 1}};
+  static int cfg[7][2] = {{2, 128}, {4, 64}, {8, 16}, {16, 16}, {32, 4}, {128, 1}, {256, 1}};
   static bool parsed = false;
   if (!parsed) {
     parsed = true;
